@@ -1,0 +1,205 @@
+/*
+ * fmmb200.h — C ABI of libfmmb200.so, the B200-native (sm_100a) build of the
+ * FMM data structures of Hu, Gumerov & Duraiswami (arXiv 1301.1704, Alg. 1-5).
+ *
+ * This is the drop-in boundary for the reference package `fmmkit`:
+ *
+ *   - the kernel plugin bound to `fmmkit.backend.kernels`
+ *     (reference: pkg/src/fmmkit/backend.py:19-27, signatures in
+ *      pkg/src/fmmkit/_ckernels.pyx:65-287 and _pykernels.py:22-197), and
+ *   - the build API `fmmkit.build_all` / `fmmkit.sort_points`
+ *     (reference: pkg/src/fmmkit/lists.py:133-187, pseudosort.py:138-151).
+ *
+ * Every entry point takes plain device pointers and element counts, is
+ * stream-ordered on the caller's `stream` (a cudaStream_t passed as void*),
+ * and returns an fmmb_status.  No torch / numpy types cross this boundary.
+ * Outputs whose size is only known on the device are allocated through the
+ * caller's allocator callback (so e.g. the PyTorch caching allocator owns
+ * them); the library's temporary workspace is stream-ordered
+ * (cudaMallocAsync) and released before the call returns.
+ *
+ * Error codes mirror the reference exception types (errors.py:4-21):
+ *   FMMB_ERR_DOMAIN   -> fmmkit.errors.DomainError   (precondition violated)
+ *   FMMB_ERR_CAPACITY -> fmmkit.errors.CapacityError (level cap / budget)
+ * fmmb_last_error() returns the message of the last failing call on a handle.
+ *
+ * Threading: a handle may be used from one host thread at a time; calls on
+ * different streams with the same handle are allowed (no shared workspace).
+ */
+#ifndef FMMB200_H
+#define FMMB200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define FMMB_API __attribute__((visibility("default")))
+#else
+#define FMMB_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FMMB_MAX_LEVEL 20 /* morton.py:18 MAX_LEVEL */
+#define FMMB_ABI_VERSION 1
+
+typedef enum fmmb_status {
+  FMMB_OK = 0,
+  FMMB_ERR_DOMAIN = 1,   /* DomainError  (errors.py:12) */
+  FMMB_ERR_CAPACITY = 2, /* CapacityError (errors.py:8)  */
+  FMMB_ERR_CUDA = 3,     /* CUDA runtime failure          */
+  FMMB_ERR_ALLOC = 4,    /* allocator callback returned NULL */
+  FMMB_ERR_ARG = 5       /* NULL handle / pointer misuse  */
+} fmmb_status;
+
+typedef struct fmmb_handle_s* fmmb_handle_t;
+
+/* Allocator callback: returns a device pointer of >= nbytes, aligned to 256 B,
+ * valid on the call's stream; NULL on failure.  Called only from the host
+ * thread that made the library call. */
+typedef void* (*fmmb_alloc_fn)(void* ctx, uint64_t nbytes);
+
+/* ---------------------------------------------------------------- lifecycle */
+FMMB_API int fmmb_abi_version(void);
+FMMB_API fmmb_status fmmb_create(int device, fmmb_handle_t* out);
+FMMB_API fmmb_status fmmb_destroy(fmmb_handle_t h);
+FMMB_API const char* fmmb_last_error(fmmb_handle_t h);
+/* number of kernel launches issued by the last call on this handle */
+FMMB_API int64_t fmmb_last_launch_count(fmmb_handle_t h);
+
+/* ------------------------------------------------------ kernel plugin level */
+
+/* spread_bits / compact_bits  (_pykernels.py:22-40, _ckernels.pyx:27-44,65-70) */
+FMMB_API fmmb_status fmmb_spread_bits(fmmb_handle_t h, const uint64_t* v, int64_t n,
+                             uint64_t* out, void* stream);
+FMMB_API fmmb_status fmmb_compact_bits(fmmb_handle_t h, const uint64_t* v, int64_t n,
+                              uint64_t* out, void* stream);
+/* interleave_coords / deinterleave_indices (_pykernels.py:43-57) */
+FMMB_API fmmb_status fmmb_interleave_coords(fmmb_handle_t h, const uint64_t* ix,
+                                   const uint64_t* iy, const uint64_t* iz,
+                                   int64_t n, uint64_t* out, void* stream);
+FMMB_API fmmb_status fmmb_deinterleave_indices(fmmb_handle_t h, const uint64_t* idx,
+                                      int64_t n, uint64_t* ix, uint64_t* iy,
+                                      uint64_t* iz, void* stream);
+
+/* encode_points(x, y, z, level) (_ckernels.pyx:85-104): truncating f64
+ * quantisation `(long long)(x * 2^level)` with an upper clamp to 2^level-1,
+ * then bit interleave.  x/y/z are strided by *_stride ELEMENTS (so a column
+ * of an (N,3) C array has stride 3).  Bit-identical to the compiled backend
+ * for every finite or non-finite input. */
+FMMB_API fmmb_status fmmb_encode_points(fmmb_handle_t h, const double* x,
+                               int64_t x_stride, const double* y,
+                               int64_t y_stride, const double* z,
+                               int64_t z_stride, int64_t n, int level,
+                               uint64_t* out, void* stream);
+
+/* assign_box_ranks(boxes, nbins) (_ckernels.pyx:107-119): dense occupancy
+ * histogram `bins[nbins]` and arrival-order rank of each point in its box.
+ * Requires boxes[i] < nbins (FMMB_ERR_DOMAIN otherwise; the reference indexes
+ * out of bounds there). `bins` and `ranks` are caller-allocated. */
+FMMB_API fmmb_status fmmb_assign_box_ranks(fmmb_handle_t h, const uint64_t* boxes,
+                                  int64_t n, int64_t nbins, int64_t* bins,
+                                  int64_t* ranks, void* stream);
+
+/* adjacent_segments(recv_boxes, src_boxes, level) (_ckernels.pyx:140-202):
+ * per receiver box, ranks into src_boxes (ascending, lower_bound semantics)
+ * of the in-grid 3x3x3 window members present in src_boxes.
+ * `bookmark` (nr+1, caller-allocated); the flat list is allocated through
+ * `alloc` with exactly *total entries. */
+FMMB_API fmmb_status fmmb_adjacent_segments(fmmb_handle_t h, const uint64_t* recv,
+                                   int64_t nr, const uint64_t* src, int64_t ns,
+                                   int level, int64_t* bookmark,
+                                   fmmb_alloc_fn alloc, void* ctx,
+                                   int64_t** list, int64_t* total,
+                                   void* stream);
+
+/* stencil_segments(recv_boxes, src_boxes, level) (_ckernels.pyx:205-287):
+ * per receiver box, ranks into src_boxes of the children of the parent's
+ * 3x3x3 window that are not in the box's own 3x3x3 window, ascending, and
+ * the i16 offset codes (dx+3)+7(dy+3)+49(dz+3).  Empty lists for level < 2. */
+FMMB_API fmmb_status fmmb_stencil_segments(fmmb_handle_t h, const uint64_t* recv,
+                                  int64_t nr, const uint64_t* src, int64_t ns,
+                                  int level, int64_t* bookmark,
+                                  fmmb_alloc_fn alloc, void* ctx,
+                                  int64_t** ranks, int16_t** codes,
+                                  int64_t* total, void* stream);
+
+/* propagate_to_parents(boxes) (lists.py:103-105): ascending unique of
+ * boxes >> 3 for an ascending input.  `out` has capacity n; *count written. */
+FMMB_API fmmb_status fmmb_propagate_to_parents(fmmb_handle_t h, const uint64_t* boxes,
+                                      int64_t n, uint64_t* out,
+                                      int64_t* count, void* stream);
+
+/* exclusive_scan(values) (scan.py:25-73): out[i] = sum(values[:i]); *total.
+ * Values must be non-negative (FMMB_ERR_DOMAIN otherwise). */
+FMMB_API fmmb_status fmmb_exclusive_scan_i64(fmmb_handle_t h, const int64_t* values,
+                                    int64_t n, int64_t* out, int64_t* total,
+                                    void* stream);
+
+/* --------------------------------------------------------- build API level */
+
+/* One sorted point set, reference layout (pseudosort.py:81-102). */
+typedef struct fmmb_point_set {
+  double* points;      /* (n, 3) f64, grouped by box, boxes ascending */
+  double* charges;     /* (n,) f64 or NULL (receivers)                 */
+  int64_t* permutation;/* (n,) sorted position -> original position    */
+  int64_t* bookmarks;  /* (k + 1,)                                      */
+  uint64_t* non_empty; /* (k,) ascending Morton indices at max level    */
+  uint64_t* boxes;     /* (n,) Morton index of each sorted point        */
+  int64_t n;
+  int64_t k;
+} fmmb_point_set;
+
+/* The whole FmmStructures bundle (lists.py:58-66).  Per-level arrays are
+ * indexed by level 0..FMMB_MAX_LEVEL; entries outside the reference's dicts
+ * (directory levels < 2 except max_level, stencil levels < 2) are NULL. */
+typedef struct fmmb_structures {
+  int32_t max_level;
+  int32_t _pad;
+  fmmb_point_set src;
+  fmmb_point_set recv;
+  /* NeighborTable (lists.py:21-30) */
+  int64_t* neighbor_bookmark; /* (k_recv + 1,) */
+  int64_t* neighbor_list;     /* (n_neighbor,) */
+  int64_t n_neighbor;
+  /* LevelDirectory (lists.py:33-42) */
+  uint64_t* dir_src[FMMB_MAX_LEVEL + 1];
+  uint64_t* dir_recv[FMMB_MAX_LEVEL + 1];
+  int64_t n_dir_src[FMMB_MAX_LEVEL + 1];
+  int64_t n_dir_recv[FMMB_MAX_LEVEL + 1];
+  /* TranslationStencils (lists.py:45-55) */
+  int64_t* st_bookmark[FMMB_MAX_LEVEL + 1]; /* (n_dir_recv[l] + 1,) */
+  int64_t* st_ranks[FMMB_MAX_LEVEL + 1];
+  int16_t* st_codes[FMMB_MAX_LEVEL + 1];
+  int64_t n_st[FMMB_MAX_LEVEL + 1];
+  /* device time of each phase, filled only if `timing` events were given */
+  int64_t n_launches;
+} fmmb_structures;
+
+/* build_all(src_points, src_charges, recv_points, max_level) (lists.py:133-187)
+ * src: (n,3) f64 C-contiguous device array; charges: (n,) f64 or NULL;
+ * recv: (m,3) f64.  All outputs are allocated through `alloc` and written to
+ * *out.  `timing` is NULL or an array of 5 cudaEvent_t recorded at the phase
+ * boundaries [start, sorted, directory, counted, end].
+ * Errors: FMMB_ERR_CAPACITY for level outside [0,20]; FMMB_ERR_DOMAIN when a
+ * point's Morton index falls outside the level grid (negative coordinates:
+ * the reference indexes its histogram out of bounds there). */
+FMMB_API fmmb_status fmmb_build_all(fmmb_handle_t h, const double* src,
+                           const double* charges, int64_t n,
+                           const double* recv, int64_t m, int level,
+                           fmmb_alloc_fn alloc, void* ctx,
+                           fmmb_structures* out, void** timing, void* stream);
+
+/* sort_points(points, charges, max_level) (pseudosort.py:138-151): the sort
+ * half of build_all for a single point set.  Outputs allocated via `alloc`. */
+FMMB_API fmmb_status fmmb_sort_points(fmmb_handle_t h, const double* points,
+                             const double* charges, int64_t n, int level,
+                             fmmb_alloc_fn alloc, void* ctx,
+                             fmmb_point_set* out, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FMMB200_H */

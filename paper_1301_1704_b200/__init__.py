@@ -1,0 +1,44 @@
+"""paper_1301_1704_b200 — B200-native (sm_100a) FMM data-structure build.
+
+Drop-in for the `fmmkit` build path (Hu, Gumerov & Duraiswami, arXiv
+1301.1704, Alg. 1-5): `build_all`, `sort_points` and the sub-builders keep the
+reference's names, arguments, errors and output layout
+(pkg/src/fmmkit/lists.py, pseudosort.py); `kernels` is a drop-in for the
+`fmmkit.backend.kernels` plugin (pkg/src/fmmkit/backend.py).  All compute is
+hand-written CUDA in libfmmb200.so behind the C ABI in include/fmmb200.h.
+"""
+
+from .errors import (
+    CapacityError,
+    DomainError,
+    FmmError,
+    InfeasiblePartitionError,
+    NativeError,
+    RoutingError,
+)
+from .lists import (
+    FmmStructures,
+    LevelDirectory,
+    NeighborTable,
+    TranslationStencils,
+    build_all,
+    build_all_device,
+    build_level_directory,
+    build_neighbor_table,
+    build_translation_stencils,
+    gather_adjacent_sources,
+    propagate_to_parents,
+)
+from .pseudosort import (
+    DEFAULT_HISTOGRAM_BUDGET,
+    MAX_LEVEL,
+    SortedPointSet,
+    build_bookmarks,
+    choose_max_level,
+    histogram_and_sort_index,
+    reorder,
+    sort_points,
+    sort_points_device,
+)
+
+__all__ = [name for name in dir() if not name.startswith("_")]

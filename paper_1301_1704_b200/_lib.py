@@ -1,0 +1,196 @@
+"""ctypes binding of libfmmb200.so (C ABI: include/fmmb200.h).
+
+The shared library is built in-tree (``paper_1301_1704_b200/libfmmb200.so``)
+by ``__graft_entry__.build()`` / ``make -C paper_1301_1704_b200/csrc``.  There
+is no fallback: if the library or a GPU is missing, every compute entry point
+raises :class:`NativeError`.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import os
+import threading
+
+import torch
+
+from .errors import CapacityError, DomainError, NativeError
+
+MAX_LEVEL = 20
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libfmmb200.so")
+
+OK, ERR_DOMAIN, ERR_CAPACITY, ERR_CUDA, ERR_ALLOC, ERR_ARG = range(6)
+
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_void_p, C.c_uint64)
+_p = C.c_void_p
+_i64 = C.c_int64
+
+
+class PointSetC(C.Structure):
+    _fields_ = [
+        ("points", _p), ("charges", _p), ("permutation", _p), ("bookmarks", _p),
+        ("non_empty", _p), ("boxes", _p), ("n", _i64), ("k", _i64),
+    ]
+
+
+_L = MAX_LEVEL + 1
+
+
+class StructuresC(C.Structure):
+    _fields_ = [
+        ("max_level", C.c_int32), ("_pad", C.c_int32),
+        ("src", PointSetC), ("recv", PointSetC),
+        ("neighbor_bookmark", _p), ("neighbor_list", _p), ("n_neighbor", _i64),
+        ("dir_src", _p * _L), ("dir_recv", _p * _L),
+        ("n_dir_src", _i64 * _L), ("n_dir_recv", _i64 * _L),
+        ("st_bookmark", _p * _L), ("st_ranks", _p * _L), ("st_codes", _p * _L),
+        ("n_st", _i64 * _L),
+        ("n_launches", _i64),
+    ]
+
+
+# (name, restype, argtypes) for every symbol in include/fmmb200.h
+SIGNATURES = [
+    ("fmmb_abi_version", C.c_int, []),
+    ("fmmb_create", C.c_int, [C.c_int, C.POINTER(_p)]),
+    ("fmmb_destroy", C.c_int, [_p]),
+    ("fmmb_last_error", C.c_char_p, [_p]),
+    ("fmmb_last_launch_count", _i64, [_p]),
+    ("fmmb_spread_bits", C.c_int, [_p, _p, _i64, _p, _p]),
+    ("fmmb_compact_bits", C.c_int, [_p, _p, _i64, _p, _p]),
+    ("fmmb_interleave_coords", C.c_int, [_p, _p, _p, _p, _i64, _p, _p]),
+    ("fmmb_deinterleave_indices", C.c_int, [_p, _p, _i64, _p, _p, _p, _p]),
+    ("fmmb_encode_points", C.c_int, [_p, _p, _i64, _p, _i64, _p, _i64, _i64, C.c_int, _p, _p]),
+    ("fmmb_assign_box_ranks", C.c_int, [_p, _p, _i64, _i64, _p, _p, _p]),
+    ("fmmb_adjacent_segments", C.c_int,
+     [_p, _p, _i64, _p, _i64, C.c_int, _p, ALLOC_FN, _p, C.POINTER(_p), C.POINTER(_i64), _p]),
+    ("fmmb_stencil_segments", C.c_int,
+     [_p, _p, _i64, _p, _i64, C.c_int, _p, ALLOC_FN, _p, C.POINTER(_p), C.POINTER(_p),
+      C.POINTER(_i64), _p]),
+    ("fmmb_propagate_to_parents", C.c_int, [_p, _p, _i64, _p, C.POINTER(_i64), _p]),
+    ("fmmb_exclusive_scan_i64", C.c_int, [_p, _p, _i64, _p, C.POINTER(_i64), _p]),
+    ("fmmb_build_all", C.c_int,
+     [_p, _p, _p, _i64, _p, _i64, C.c_int, ALLOC_FN, _p, C.POINTER(StructuresC), _p, _p]),
+    ("fmmb_sort_points", C.c_int,
+     [_p, _p, _p, _i64, C.c_int, ALLOC_FN, _p, C.POINTER(PointSetC), _p]),
+]
+
+_lib = None
+_lib_lock = threading.Lock()
+_handles: dict[int, int] = {}
+
+
+def load(path: str = LIB_PATH):
+    """Load the CUDA library (raises NativeError if it is missing)."""
+    global _lib
+    with _lib_lock:
+        if _lib is None:
+            if not os.path.exists(path):
+                raise NativeError(
+                    f"{path} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'`"
+                )
+            lib = C.CDLL(path)
+            for name, res, args in SIGNATURES:
+                fn = getattr(lib, name)
+                fn.restype = res
+                fn.argtypes = args
+            _lib = lib
+    return _lib
+
+
+def exported_symbols() -> list[str]:
+    return [name for name, _, _ in SIGNATURES]
+
+
+def device_of(device=None) -> torch.device:
+    if device is None:
+        if not torch.cuda.is_available():
+            raise NativeError("no CUDA device: the B200 build has no CPU fallback")
+        return torch.device("cuda", torch.cuda.current_device())
+    dev = torch.device(device)
+    if dev.type != "cuda":
+        raise NativeError(f"device {dev} is not a CUDA device")
+    if dev.index is None:
+        dev = torch.device("cuda", torch.cuda.current_device())
+    return dev
+
+
+def handle(dev: torch.device) -> int:
+    lib = load()
+    idx = dev.index
+    h = _handles.get(idx)
+    if h is None:
+        out = C.c_void_p()
+        st = lib.fmmb_create(idx, C.byref(out))
+        if st != OK:
+            raise NativeError(f"fmmb_create(device={idx}) failed with status {st}")
+        h = out.value
+        _handles[idx] = h
+    return h
+
+
+def stream_of(dev: torch.device) -> int:
+    return torch.cuda.current_stream(dev).cuda_stream
+
+
+def check(st: int, h: int) -> None:
+    if st == OK:
+        return
+    msg = load().fmmb_last_error(h).decode(errors="replace")
+    if st == ERR_DOMAIN:
+        raise DomainError(msg)
+    if st == ERR_CAPACITY:
+        raise CapacityError(msg)
+    raise NativeError(f"libfmmb200 status {st}: {msg}")
+
+
+class Allocator:
+    """Allocator callback backed by the PyTorch caching allocator.
+
+    Every block handed to the library is a uint8 CUDA tensor kept in
+    ``self.blocks`` (so the outputs' lifetime is torch's)."""
+
+    def __init__(self, dev: torch.device):
+        self.dev = dev
+        self.blocks: list[torch.Tensor] = []
+        self.error: BaseException | None = None
+
+        def _alloc(_ctx, nbytes):
+            try:
+                t = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=self.dev)
+            except BaseException as e:  # noqa: BLE001 - reported after the call
+                self.error = e
+                return None
+            self.blocks.append(t)
+            return t.data_ptr()
+
+        self.fn = ALLOC_FN(_alloc)
+
+    def block_of(self, ptr: int) -> tuple[torch.Tensor, int]:
+        for b in self.blocks:
+            base = b.data_ptr()
+            if base <= ptr < base + b.numel() or (ptr == base):
+                return b, ptr - base
+        raise NativeError(f"pointer {ptr:#x} is not in any allocated block")
+
+
+_TORCH_DTYPES = {
+    "f8": torch.float64, "i8": torch.int64, "u8": torch.uint64, "i2": torch.int16,
+    "u4": torch.uint32, "i4": torch.int32,
+}
+
+
+def view(alloc: Allocator, ptr: int | None, count: int, dtype: str, shape=None) -> torch.Tensor:
+    """Typed device view of `count` elements at `ptr` inside an allocated block."""
+    tdt = _TORCH_DTYPES[dtype]
+    if not ptr or count == 0:
+        t = torch.empty(0, dtype=tdt, device=alloc.dev)
+        return t.reshape(shape if shape is not None else (0,)) if shape is not None else t
+    block, off = alloc.block_of(ptr)
+    size = torch.empty(0, dtype=tdt).element_size()
+    raw = block[off: off + count * size]
+    t = raw.view(tdt)
+    if shape is not None:
+        t = t.view(*shape)
+    return t

@@ -1,0 +1,510 @@
+// libfmmb200: C-ABI entry points for the fused build (fmmb_build_all,
+// fmmb_sort_points) and the handle lifecycle.  Host orchestration of the
+// sm_100a kernels in sort.cuh / finalize.cuh / lists.cuh.
+//
+// build_all (reference lists.py:133-187) runs as two stream-ordered phases:
+//   A: encode+histogram -> P radix passes -> gather/bookmarks/bitmap_L ->
+//      bitmap pyramid -> rank directory + level directory -> list counts ->
+//      segmented scan into the CSR bookmarks
+//   -- one device->host read of the sizes (K per level, |E2|, |E4_l|) --
+//   B: list write pass into exactly-sized outputs.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.h"
+#include "common.cuh"
+#include "finalize.cuh"
+#include "lists.cuh"
+#include "sort.cuh"
+
+using namespace fmmb;
+
+// ------------------------------------------------------------------ handle
+fmmb_status fmmb_fail(fmmb_handle_t h, fmmb_status st, const char* fmt, ...) {
+  if (h) {
+    char buf[1024];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    h->err = buf;
+  }
+  return st;
+}
+
+extern "C" int fmmb_abi_version(void) { return FMMB_ABI_VERSION; }
+
+extern "C" fmmb_status fmmb_create(int device, fmmb_handle_t* out) {
+  if (!out) return FMMB_ERR_ARG;
+  *out = nullptr;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev)
+    return FMMB_ERR_CUDA;
+  auto* h = new fmmb_handle_s();
+  h->device = device;
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, device) != cudaSuccess) {
+    delete h;
+    return FMMB_ERR_CUDA;
+  }
+  h->num_sms = prop.multiProcessorCount;
+  h->pinned = nullptr;
+  if (cudaSetDevice(device) != cudaSuccess ||
+      cudaMallocHost(&h->pinned, kPinnedBytes) != cudaSuccess) {
+    delete h;
+    return FMMB_ERR_CUDA;
+  }
+  // stream-ordered pool: keep freed workspace for reuse across calls
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  // opt-in dynamic shared memory for the big-tile kernels
+  cudaFuncSetAttribute(k_onesweep<uint32_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)onesweep_smem_bytes(4));
+  cudaFuncSetAttribute(k_onesweep<uint32_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)onesweep_smem_bytes(4));
+  cudaFuncSetAttribute(k_onesweep<uint64_t, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)onesweep_smem_bytes(8));
+  cudaFuncSetAttribute(k_onesweep<uint64_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)onesweep_smem_bytes(8));
+  cudaFuncSetAttribute(k_gather<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)gather_smem_bytes());
+  cudaFuncSetAttribute(k_gather<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)gather_smem_bytes());
+  if (cudaGetLastError() != cudaSuccess) {
+    cudaFreeHost(h->pinned);
+    delete h;
+    return FMMB_ERR_CUDA;
+  }
+  *out = h;
+  return FMMB_OK;
+}
+
+extern "C" fmmb_status fmmb_destroy(fmmb_handle_t h) {
+  if (!h) return FMMB_ERR_ARG;
+  cudaSetDevice(h->device);
+  if (h->pinned) cudaFreeHost(h->pinned);
+  delete h;
+  return FMMB_OK;
+}
+
+extern "C" const char* fmmb_last_error(fmmb_handle_t h) {
+  return h ? h->err.c_str() : "null handle";
+}
+
+extern "C" int64_t fmmb_last_launch_count(fmmb_handle_t h) { return h ? h->launches : -1; }
+
+int lists_lmin_host(int L) { return L >= 2 ? 2 : L; }
+
+// --------------------------------------------------------------- arenas --
+namespace {
+
+struct Carver {  // sub-allocates 256-B aligned slices of one allocation
+  size_t off = 0;
+  template <typename T>
+  size_t take(int64_t count) {
+    const size_t at = off;
+    off += ((size_t)std::max<int64_t>(count, 0) * sizeof(T) + 255) & ~(size_t)255;
+    return at;
+  }
+};
+
+inline int64_t cap_level(int64_t count, int level) {  // min(count, 8^level)
+  if (3 * level >= 62) return count;
+  return std::min<int64_t>(count, 1ll << (3 * level));
+}
+
+inline int64_t level_words(int level) {  // u64 words of a level bitmap
+  const int64_t bits = 1ll << (3 * level);
+  return std::max<int64_t>(1, bits / 64);
+}
+
+}  // namespace
+
+// Bitmap path limit: the level-L occupancy bitmap of one set is 8^L/8 bytes.
+bool fmmb_bitmap_ok(int level, int64_t n_total) {
+  if (level > 12) return false;
+  const double bytes = std::ldexp(1.0, 3 * level) / 8.0;
+  return bytes <= std::max(64.0 * 1024 * 1024, 4.0 * 8.0 * (double)n_total);
+}
+
+// --------------------------------------------------------------- build ---
+namespace {
+
+struct BuildPlanHost {  // mirrored in the pinned readback block
+  int64_t ktot[kMaxSegs];
+  int64_t seg_totals[kMaxLevel + 1];
+  int64_t kinfo[2];
+  uint32_t err;
+};
+
+template <typename KeyT>
+fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int64_t n,
+                       const double* recv, int64_t m, int L, fmmb_alloc_fn alloc,
+                       void* ctx, fmmb_structures* out, cudaEvent_t* ev,
+                       cudaStream_t s, bool lists) {
+  const int64_t tot = n + m;
+  const int npass = sort_passes(L);
+  const int64_t sort_tiles = ceil_div(tot, kSortTile);
+  const int64_t gather_tiles = ceil_div(tot, kGTile);
+  const int stride = L + 1;
+
+  // bitmap segment layout: seg = set*(L+1)+l, each starting on a rank tile
+  RankParams rp{};
+  rp.nseg = 2 * stride;
+  int64_t words = 0, tiles = 0;
+  for (int set = 0; set < 2; ++set)
+    for (int l = 0; l <= L; ++l) {
+      const int sg = set * stride + l;
+      rp.word_off[sg] = words;
+      rp.nwords[sg] = level_words(l);
+      rp.tile_off[sg] = tiles;
+      const int64_t t = ceil_div(rp.nwords[sg], kRTileWords);
+      tiles += t;
+      words += t * kRTileWords;
+    }
+  rp.tile_off[rp.nseg] = tiles;
+  const int64_t bmp_words = lists ? words : 0, rank_tiles = lists ? tiles : 0;
+
+  // list count segments: capacity from min(m, 8^l)
+  int64_t cnt_cap = 0;
+  for (int sg = 0; sg <= kMaxLevel; ++sg) {
+    int64_t len = 0;
+    if (sg == 0) len = cap_level(m, L) + 1;
+    else if (sg >= 2 && sg <= L) len = cap_level(m, sg) + 1;
+    cnt_cap += round_up(len, kScanTile);
+  }
+  const int64_t scan_tiles_cap = cnt_cap / kScanTile;
+
+  // ---- workspace: [zeroed control | rest]
+  Carver z;
+  const size_t o_hist = z.take<uint32_t>(npass * kBins);
+  const size_t o_tc = z.take<uint32_t>(16);  // tile counters
+  const size_t o_sst = z.take<uint64_t>((int64_t)npass * sort_tiles * kBins);
+  const size_t o_gst = z.take<uint64_t>(gather_tiles);
+  const size_t o_rst = z.take<uint64_t>(rank_tiles);
+  const size_t o_lst = z.take<uint64_t>(scan_tiles_cap);
+  const size_t o_plan = z.take<BuildPlanHost>(1);
+  const size_t o_bmp = z.take<uint64_t>(bmp_words);
+  const size_t zero_bytes = z.off;
+  const size_t o_dir = z.take<uint32_t>(bmp_words);
+  const size_t o_ka = z.take<KeyT>(tot), o_kb = z.take<KeyT>(tot);
+  const size_t o_va = z.take<uint32_t>(tot), o_vb = z.take<uint32_t>(tot);
+  const size_t o_lowkeys = z.take<uint64_t>(2 * (1 + 8));  // levels 0,1 keys
+  const size_t o_cnt = z.take<uint32_t>(cnt_cap);
+  char* ws = nullptr;
+  if (cudaMallocAsync((void**)&ws, z.off, s) != cudaSuccess)
+    return fmmb_fail(h, FMMB_ERR_CUDA, "workspace allocation of %zu bytes failed", z.off);
+  auto W = [&](size_t o) { return (void*)(ws + o); };
+  uint32_t* hist = (uint32_t*)W(o_hist);
+  uint32_t* tc = (uint32_t*)W(o_tc);
+  BuildPlanHost* dplan = (BuildPlanHost*)W(o_plan);
+  uint64_t* bmp = (uint64_t*)W(o_bmp);
+  uint32_t* dir = (uint32_t*)W(o_dir);
+
+  // ---- output arena A (sizes known before the build)
+  Carver a;
+  const size_t a_pts = a.take<double>(3 * tot);
+  const size_t a_q = a.take<double>(q ? n : 0);
+  const size_t a_perm = a.take<int64_t>(tot);
+  const size_t a_boxes = a.take<uint64_t>(tot);
+  const size_t a_ne = a.take<uint64_t>(tot);
+  const size_t a_bm = a.take<int64_t>(tot + 2);
+  size_t a_dir[2][kMaxLevel + 1] = {};
+  size_t a_lbm[kMaxLevel + 1] = {};
+  if (lists) {
+    for (int l = 2; l < L; ++l) {
+      a_dir[0][l] = a.take<uint64_t>(cap_level(n, l));
+      a_dir[1][l] = a.take<uint64_t>(cap_level(m, l));
+    }
+    a_lbm[0] = a.take<int64_t>(cap_level(m, L) + 1);
+    for (int l = 2; l <= L; ++l) a_lbm[l] = a.take<int64_t>(cap_level(m, l) + 1);
+  }
+  char* arena = (char*)alloc(ctx, a.off);
+  if (!arena) {
+    cudaFreeAsync(ws, s);
+    return fmmb_fail(h, FMMB_ERR_ALLOC, "output allocation of %zu bytes failed", a.off);
+  }
+  auto A = [&](size_t o) { return (void*)(arena + o); };
+  double* pts_out = (double*)A(a_pts);
+  int64_t* bm_out = (int64_t*)A(a_bm);
+  uint64_t* ne_out = (uint64_t*)A(a_ne);
+
+  int64_t launches = 0;
+#define FMMB_LAUNCHED() \
+  do {                  \
+    ++launches;         \
+  } while (0)
+
+  if (ev) cudaEventRecord(ev[0], s);
+  cudaMemsetAsync(ws, 0, zero_bytes, s);
+  if (tot == 0) cudaMemsetAsync(bm_out, 0, 2 * sizeof(int64_t), s);
+
+  // ---- K1/K2: encode + radix sort
+  KeyT* ka = (KeyT*)W(o_ka);
+  KeyT* kb = (KeyT*)W(o_kb);
+  uint32_t* va = (uint32_t*)W(o_va);
+  uint32_t* vb = (uint32_t*)W(o_vb);
+  if (tot > 0) {
+    const int eg = (int)std::min<int64_t>(ceil_div(tot, kSortThreads), (int64_t)h->num_sms * 8);
+    k_encode_hist<KeyT><<<eg, kSortThreads, 0, s>>>(src, n, recv, m, L, npass, ka, hist,
+                                                    &dplan->err);
+    FMMB_LAUNCHED();
+    uint64_t* sst = (uint64_t*)W(o_sst);
+    const size_t smem = onesweep_smem_bytes(sizeof(KeyT));
+    for (int ps = 0; ps < npass; ++ps) {
+      uint64_t* st = sst + (size_t)ps * sort_tiles * kBins;
+      if (ps == 0)
+        k_onesweep<KeyT, true><<<(unsigned)sort_tiles, kSortThreads, smem, s>>>(
+            ka, nullptr, kb, vb, tot, 0, hist, st, tc + ps);
+      else
+        k_onesweep<KeyT, false><<<(unsigned)sort_tiles, kSortThreads, smem, s>>>(
+            ka, va, kb, vb, tot, kRadixBits * ps, hist + ps * kBins, st, tc + ps);
+      FMMB_LAUNCHED();
+      std::swap(ka, kb);
+      std::swap(va, vb);
+    }
+    // ---- K3/K4: gather + bookmarks + level-L bitmaps
+    k_gather<KeyT><<<(unsigned)gather_tiles, kGThreads, gather_smem_bytes(), s>>>(
+        ka, va, n, m, L, src, q, recv, pts_out, q ? (double*)A(a_q) : nullptr,
+        (int64_t*)A(a_perm), (uint64_t*)A(a_boxes), ne_out, bm_out,
+        lists ? (unsigned long long*)(bmp + rp.word_off[L]) : nullptr,
+        lists ? (unsigned long long*)(bmp + rp.word_off[stride + L]) : nullptr,
+        (uint64_t*)W(o_gst), tc + 8, dplan->kinfo);
+    FMMB_LAUNCHED();
+  }
+  if (ev) cudaEventRecord(ev[1], s);
+
+  // ---- K5: bitmap pyramid (big levels one launch each, the rest in one CTA)
+  int l = lists ? L : 0;
+  while (l >= 1 && level_words(l - 1) > 4096) {
+    const int64_t nc = level_words(l - 1);
+    k_pyramid<<<(unsigned)ceil_div(2 * nc, 256), 256, 0, s>>>(
+        bmp + rp.word_off[l], bmp + rp.word_off[l - 1], bmp + rp.word_off[stride + l],
+        bmp + rp.word_off[stride + l - 1], nc);
+    FMMB_LAUNCHED();
+    --l;
+  }
+  if (l >= 1) {
+    PyramidTail pt{};
+    for (int k = 0; k <= L; ++k) {
+      pt.lvl[0][k] = bmp + rp.word_off[k];
+      pt.lvl[1][k] = bmp + rp.word_off[stride + k];
+      pt.nwords[k] = level_words(k);
+    }
+    pt.from_level = l;
+    k_pyramid_tail<<<1, 1024, 0, s>>>(pt);
+    FMMB_LAUNCHED();
+  }
+  // ---- rank directory, totals and per-level directory keys
+  rp.bmp = bmp;
+  rp.dir = dir;
+  rp.states = (uint64_t*)W(o_rst);
+  rp.tile_counter = tc + 9;
+  rp.totals = dplan->ktot;
+  uint64_t* lowkeys = (uint64_t*)W(o_lowkeys);
+  for (int set = 0; set < 2; ++set)
+    for (int k = 0; k <= L; ++k) {
+      uint64_t* dst = nullptr;
+      if (k < L) {
+        if (k == 0) dst = lowkeys + set * 9;
+        else if (k == 1) dst = lowkeys + set * 9 + 1;
+        else if (lists) dst = (uint64_t*)A(a_dir[set][k]);
+      }
+      rp.keys_out[set * stride + k] = dst;
+    }
+  if (lists) {
+    k_rank<<<(unsigned)rank_tiles, kRThreads, 0, s>>>(rp);
+    FMMB_LAUNCHED();
+  }
+  if (ev) cudaEventRecord(ev[2], s);
+
+  ListsParams lp{};
+  int64_t nwork_cap = 0;
+  if (lists) {
+    lp.level = L;
+    lp.ktot = dplan->ktot;
+    lp.bmp = bmp;
+    lp.dir = dir;
+    for (int set = 0; set < 2; ++set)
+      for (int k = 0; k <= L; ++k) lp.bmp_off[set][k] = rp.word_off[set * stride + k];
+    for (int k = 0; k < L; ++k) lp.rkeys[k] = rp.keys_out[stride + k];
+    lp.counts = (uint32_t*)W(o_cnt);
+    lp.bm[0] = (int64_t*)A(a_lbm[0]);
+    for (int k = 2; k <= L; ++k) lp.bm[k] = (int64_t*)A(a_lbm[k]);
+    for (int k = std::max(1, lists_lmin_host(L)); k <= L; ++k) nwork_cap += cap_level(m, k - 1);
+    if (L == 0) nwork_cap = 1;
+    const int lgrid = (int)std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * 16));
+    k_lists<false><<<lgrid, kLThreads, 0, s>>>(lp);
+    FMMB_LAUNCHED();
+    k_lists_scan<<<(unsigned)std::max<int64_t>(1, scan_tiles_cap), kScanThreads, 0, s>>>(
+        lp, (uint64_t*)W(o_lst), tc + 10, dplan->seg_totals);
+    FMMB_LAUNCHED();
+  }
+  if (ev) cudaEventRecord(ev[3], s);
+
+  // ---- sizes back to the host (the build's single synchronisation)
+  BuildPlanHost* hp = (BuildPlanHost*)h->pinned;
+  cudaMemcpyAsync(hp, dplan, sizeof(BuildPlanHost), cudaMemcpyDeviceToHost, s);
+  cudaError_t ce = cudaStreamSynchronize(s);
+  if (ce != cudaSuccess) {
+    cudaFreeAsync(ws, s);
+    return fmmb_fail(h, FMMB_ERR_CUDA, "build phase A failed: %s", cudaGetErrorString(ce));
+  }
+  if (hp->err) {
+    cudaFreeAsync(ws, s);
+    return fmmb_fail(h, FMMB_ERR_DOMAIN,
+                     "a point's Morton index lies outside the level-%d grid "
+                     "(coordinates must lie in the unit cube)", L);
+  }
+  const int64_t ks = lists ? hp->ktot[L] : (n > 0 ? hp->kinfo[0] : 0);
+  const int64_t kr = lists ? hp->ktot[stride + L] : 0;
+  if (lists && tot > 0 && (hp->kinfo[0] != ks || (m > 0 && hp->kinfo[1] != ks + kr))) {
+    cudaFreeAsync(ws, s);
+    return fmmb_fail(h, FMMB_ERR_CUDA, "internal: box counts disagree (%lld/%lld vs %lld/%lld)",
+                     (long long)hp->kinfo[0], (long long)hp->kinfo[1], (long long)ks,
+                     (long long)kr);
+  }
+
+  // ---- fill the output descriptor (phase A part)
+  memset(out, 0, sizeof(*out));
+  out->max_level = L;
+  out->src.points = pts_out;
+  out->src.charges = q ? (double*)A(a_q) : nullptr;
+  out->src.permutation = (int64_t*)A(a_perm);
+  out->src.boxes = (uint64_t*)A(a_boxes);
+  out->src.non_empty = ne_out;
+  out->src.bookmarks = bm_out;
+  out->src.n = n;
+  out->src.k = ks;
+  out->recv.points = pts_out + 3 * n;
+  out->recv.charges = nullptr;
+  out->recv.permutation = (int64_t*)A(a_perm) + n;
+  out->recv.boxes = (uint64_t*)A(a_boxes) + n;
+  out->recv.non_empty = ne_out + ks;
+  out->recv.bookmarks = bm_out + ks + 1;
+  out->recv.n = m;
+  out->recv.k = kr;
+
+  if (lists) {
+    // ---- phase B: exactly-sized list outputs, then the write pass
+    const int64_t e2 = hp->seg_totals[0];
+    Carver b;
+    const size_t b_e2 = b.take<int64_t>(e2);
+    size_t b_r[kMaxLevel + 1] = {}, b_c[kMaxLevel + 1] = {};
+    for (int k = 2; k <= L; ++k) {
+      b_r[k] = b.take<int64_t>(hp->seg_totals[k]);
+      b_c[k] = b.take<int16_t>(hp->seg_totals[k]);
+    }
+    char* arena_b = (char*)alloc(ctx, std::max<size_t>(b.off, 256));
+    if (!arena_b) {
+      cudaFreeAsync(ws, s);
+      return fmmb_fail(h, FMMB_ERR_ALLOC, "list allocation of %zu bytes failed", b.off);
+    }
+    lp.ranks_out[0] = (int64_t*)(arena_b + b_e2);
+    for (int k = 2; k <= L; ++k) {
+      lp.ranks_out[k] = (int64_t*)(arena_b + b_r[k]);
+      lp.codes_out[k] = (int16_t*)(arena_b + b_c[k]);
+    }
+    const int lgrid = (int)std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * 16));
+    k_lists<true><<<lgrid, kLThreads, 0, s>>>(lp);
+    FMMB_LAUNCHED();
+
+    out->neighbor_bookmark = lp.bm[0];
+    out->neighbor_list = lp.ranks_out[0];
+    out->n_neighbor = e2;
+    out->dir_src[L] = ne_out;
+    out->n_dir_src[L] = ks;
+    out->dir_recv[L] = ne_out + ks;
+    out->n_dir_recv[L] = kr;
+    for (int k = 2; k < L; ++k) {
+      out->dir_src[k] = (uint64_t*)A(a_dir[0][k]);
+      out->dir_recv[k] = (uint64_t*)A(a_dir[1][k]);
+      out->n_dir_src[k] = hp->ktot[k];
+      out->n_dir_recv[k] = hp->ktot[stride + k];
+    }
+    for (int k = 2; k <= L; ++k) {
+      out->st_bookmark[k] = lp.bm[k];
+      out->st_ranks[k] = lp.ranks_out[k];
+      out->st_codes[k] = lp.codes_out[k];
+      out->n_st[k] = hp->seg_totals[k];
+    }
+  }
+  if (ev) cudaEventRecord(ev[4], s);
+  cudaFreeAsync(ws, s);
+  out->n_launches = launches;
+  h->launches = launches;
+  ce = cudaGetLastError();
+  if (ce != cudaSuccess)
+    return fmmb_fail(h, FMMB_ERR_CUDA, "build launch failed: %s", cudaGetErrorString(ce));
+#undef FMMB_LAUNCHED
+  return FMMB_OK;
+}
+
+fmmb_status check_build_args(fmmb_handle_t h, const double* src, int64_t n, const double* recv,
+                             int64_t m, int level, fmmb_alloc_fn alloc, bool lists) {
+  if (!h) return FMMB_ERR_ARG;
+  if (level < 0 || level > kMaxLevel)
+    return fmmb_fail(h, FMMB_ERR_CAPACITY, "max_level %d outside [0, %d]", level, kMaxLevel);
+  if (n < 0 || m < 0 || (n > 0 && !src) || (m > 0 && !recv) || !alloc)
+    return fmmb_fail(h, FMMB_ERR_ARG, "invalid arguments");
+  if (n + m >= (1ll << 31))
+    return fmmb_fail(h, FMMB_ERR_CAPACITY, "n + m = %lld exceeds 2^31 - 1 points per device",
+                     (long long)(n + m));
+  if (lists && !fmmb_bitmap_ok(level, n + m))
+    return fmmb_fail(h, FMMB_ERR_CAPACITY,
+                     "level %d occupancy bitmaps exceed the device budget for %lld points",
+                     level, (long long)(n + m));
+  return FMMB_OK;
+}
+
+}  // namespace
+
+
+extern "C" fmmb_status fmmb_build_all(fmmb_handle_t h, const double* src, const double* charges,
+                                      int64_t n, const double* recv, int64_t m, int level,
+                                      fmmb_alloc_fn alloc, void* ctx, fmmb_structures* out,
+                                      void** timing, void* stream) {
+  fmmb_status st = check_build_args(h, src, n, recv, m, level, alloc, true);
+  if (st != FMMB_OK) return st;
+  if (!out) return FMMB_ERR_ARG;
+  cudaSetDevice(h->device);
+  cudaStream_t s = (cudaStream_t)stream;
+  cudaEvent_t* ev = (cudaEvent_t*)timing;
+  if (sort_key_bits(level) <= 32)
+    return build_impl<uint32_t>(h, src, charges, n, recv, m, level, alloc, ctx, out, ev, s, true);
+  return build_impl<uint64_t>(h, src, charges, n, recv, m, level, alloc, ctx, out, ev, s, true);
+}
+
+extern "C" fmmb_status fmmb_sort_points(fmmb_handle_t h, const double* points,
+                                        const double* charges, int64_t n, int level,
+                                        fmmb_alloc_fn alloc, void* ctx, fmmb_point_set* out,
+                                        void* stream) {
+  fmmb_status st = check_build_args(h, points, n, nullptr, 0, level, alloc, false);
+  if (st != FMMB_OK) return st;
+  if (!out) return FMMB_ERR_ARG;
+  cudaSetDevice(h->device);
+  fmmb_structures tmp;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (sort_key_bits(level) <= 32)
+    st = build_impl<uint32_t>(h, points, charges, n, nullptr, 0, level, alloc, ctx, &tmp,
+                              nullptr, s, false);
+  else
+    st = build_impl<uint64_t>(h, points, charges, n, nullptr, 0, level, alloc, ctx, &tmp,
+                              nullptr, s, false);
+  if (st == FMMB_OK) *out = tmp.src;
+  return st;
+}
+
+#include "plugin.cuh"

@@ -1,0 +1,21 @@
+// Host-side internals shared by the libfmmb200 translation units.
+#pragma once
+#include <stdint.h>
+
+#include <string>
+
+#include "../../include/fmmb200.h"
+
+struct fmmb_handle_s {
+  int device = 0;
+  int num_sms = 148;
+  void* pinned = nullptr;  // small pinned block for size read-back
+  int64_t launches = 0;
+  std::string err;
+};
+
+constexpr size_t kPinnedBytes = 1 << 16;
+
+fmmb_status fmmb_fail(fmmb_handle_t h, fmmb_status st, const char* fmt, ...);
+bool fmmb_bitmap_ok(int level, int64_t n_total);
+int lists_lmin_host(int L);

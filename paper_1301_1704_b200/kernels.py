@@ -1,0 +1,275 @@
+"""Drop-in for the reference kernel plugin `fmmkit.backend.kernels`.
+
+Same module surface as pkg/src/fmmkit/_ckernels.pyx and _pykernels.py
+(IS_COMPILED, spread_bits, compact_bits, interleave_coords,
+deinterleave_indices, encode_points, assign_box_ranks,
+assign_box_ranks_atomic, adjacent_segments, stencil_segments, near_field,
+direct_potentials), every function computed by libfmmb200 on the GPU.
+numpy in -> numpy out (the reference contract); CUDA tensors in -> CUDA
+tensors out.  Bind it into the reference with `install()` (the reference's
+own swap mechanism is plain assignment, cli.py:263-266).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+
+from . import _host, _lib
+from .errors import DomainError
+
+IS_COMPILED = True  # backend.backend_name() reports "compiled" (backend.py:30-32)
+
+
+def _dev_u64(a, dev):
+    return _host.to_device(a, dev, torch.uint64, (-1,))
+
+
+def _out(t: torch.Tensor, device_out: bool):
+    return t if device_out else t.cpu().numpy()
+
+
+def _call(fn_name: str, dev, *args):
+    lib = _lib.load()
+    h = _lib.handle(dev)
+    st = getattr(lib, fn_name)(h, *args, _lib.stream_of(dev))
+    _lib.check(st, h)
+
+
+def _ptr(t: torch.Tensor):
+    return t.data_ptr() if t.numel() else None
+
+
+# ----------------------------------------------------------- bit dilation
+def _unary_u64(fn_name: str, v):
+    dev = _host.pick_device(v)
+    dout = _host.is_device_input(v)
+    x = _dev_u64(v, dev)
+    o = torch.empty_like(x)
+    _call(fn_name, dev, _ptr(x), x.numel(), _ptr(o))
+    return _out(o, dout)
+
+
+def spread_bits(v):
+    """Insert two zero bits between each of the low 21 bits (_pykernels.py:22-30)."""
+    return _unary_u64("fmmb_spread_bits", v)
+
+
+def compact_bits(v):
+    """Inverse of spread_bits on bits 3k (_pykernels.py:33-40)."""
+    return _unary_u64("fmmb_compact_bits", v)
+
+
+def interleave_coords(ix, iy, iz):
+    """Morton index from box coordinates (_pykernels.py:43-48)."""
+    dev = _host.pick_device(ix, iy, iz)
+    dout = _host.is_device_input(ix, iy, iz)
+    xs = [_dev_u64(a, dev) for a in (ix, iy, iz)]
+    n = xs[0].numel()
+    if any(t.numel() != n for t in xs):
+        raise DomainError("interleave_coords: coordinate arrays differ in length")
+    o = torch.empty(n, dtype=torch.uint64, device=dev)
+    _call("fmmb_interleave_coords", dev, *[_ptr(t) for t in xs], n, _ptr(o))
+    return _out(o, dout)
+
+
+def deinterleave_indices(idx):
+    """(ix, iy, iz) from Morton indices (_pykernels.py:51-57)."""
+    dev = _host.pick_device(idx)
+    dout = _host.is_device_input(idx)
+    k = _dev_u64(idx, dev)
+    outs = [torch.empty_like(k) for _ in range(3)]
+    _call("fmmb_deinterleave_indices", dev, _ptr(k), k.numel(), *[_ptr(t) for t in outs])
+    return tuple(_out(t, dout) for t in outs)
+
+
+# --------------------------------------------------------------- encoding
+def encode_points_device(x: torch.Tensor, y: torch.Tensor, z: torch.Tensor, level: int):
+    """Morton keys of (possibly strided) f64 CUDA columns."""
+    dev = _lib.device_of(x.device)
+    n = x.numel()
+    cols = []
+    for c in (x, y, z):
+        if c.dtype != torch.float64 or c.dim() != 1:
+            c = c.reshape(-1).to(torch.float64)
+        cols.append(c)
+    o = torch.empty(n, dtype=torch.uint64, device=dev)
+    args = []
+    for c in cols:
+        args += [_ptr(c), c.stride(0) if c.numel() else 1]
+    _call("fmmb_encode_points", dev, *args, n, level, _ptr(o))
+    return o
+
+
+def encode_points(x, y, z, level: int):
+    """Morton index of the level-`level` box containing each point
+    (_ckernels.pyx:85-104): truncating f64 quantisation, upper clamp."""
+    dev = _host.pick_device(x, y, z)
+    dout = _host.is_device_input(x, y, z)
+    cols = [_host.to_device(c, dev, torch.float64, (-1,)) for c in (x, y, z)]
+    if not (cols[0].numel() == cols[1].numel() == cols[2].numel()):
+        raise DomainError("encode_points: coordinate arrays differ in length")
+    return _out(encode_points_device(*cols, level), dout)
+
+
+# ---------------------------------------------------------- rank assignment
+def assign_box_ranks_device(boxes: torch.Tensor, nbins: int):
+    dev = _lib.device_of(boxes.device)
+    n = boxes.numel()
+    bins = torch.empty(nbins, dtype=torch.int64, device=dev)
+    ranks = torch.empty(n, dtype=torch.int64, device=dev)
+    _call("fmmb_assign_box_ranks", dev, _ptr(boxes), n, nbins, _ptr(bins), _ptr(ranks))
+    return bins, ranks
+
+
+def assign_box_ranks(boxes, nbins: int):
+    """Dense occupancy histogram plus each point's arrival rank within its box
+    (_ckernels.pyx:107-119)."""
+    dev = _host.pick_device(boxes)
+    dout = _host.is_device_input(boxes)
+    b = _dev_u64(boxes, dev)
+    bins, ranks = assign_box_ranks_device(b, int(nbins))
+    return _out(bins, dout), _out(ranks, dout)
+
+
+def assign_box_ranks_atomic(boxes, nbins: int, threads: int = 1):
+    """The reference's shared-counter variant (_ckernels.pyx:122-137) allows
+    any within-box order; the deterministic order is a legal one
+    (_pykernels.py:90-95 makes the same choice)."""
+    return assign_box_ranks(boxes, nbins)
+
+
+# ---------------------------------------------------------- list builders
+def _segments(fn_name: str, recv_boxes, src_boxes, level: int, stencil: bool):
+    dev = _host.pick_device(recv_boxes, src_boxes)
+    dout = _host.is_device_input(recv_boxes, src_boxes)
+    r = _dev_u64(recv_boxes, dev)
+    s = _dev_u64(src_boxes, dev)
+    nr, ns = r.numel(), s.numel()
+    bm = torch.empty(nr + 1, dtype=torch.int64, device=dev)
+    alloc = _lib.Allocator(dev)
+    lst = C.c_void_p()
+    codes = C.c_void_p()
+    total = C.c_int64()
+    lib = _lib.load()
+    h = _lib.handle(dev)
+    if stencil:
+        st = lib.fmmb_stencil_segments(h, _ptr(r), nr, _ptr(s), ns, level, _ptr(bm), alloc.fn,
+                                       None, C.byref(lst), C.byref(codes), C.byref(total),
+                                       _lib.stream_of(dev))
+    else:
+        st = lib.fmmb_adjacent_segments(h, _ptr(r), nr, _ptr(s), ns, level, _ptr(bm), alloc.fn,
+                                        None, C.byref(lst), C.byref(total), _lib.stream_of(dev))
+    if alloc.error is not None:
+        raise alloc.error
+    _lib.check(st, h)
+    e = int(total.value)
+    flat = _lib.view(alloc, lst.value, e, "i8")
+    if not stencil:
+        return _out(bm, dout), _out(flat, dout)
+    cd = _lib.view(alloc, codes.value, e, "i2")
+    return _out(bm, dout), _out(flat, dout), _out(cd, dout)
+
+
+def adjacent_segments(recv_boxes, src_boxes, level: int):
+    """Per receiver box, the ranks into src_boxes of its in-grid 3x3x3 window
+    members present in src_boxes, ascending (_ckernels.pyx:172-202)."""
+    return _segments("fmmb_adjacent_segments", recv_boxes, src_boxes, level, False)
+
+
+def stencil_segments(recv_boxes, src_boxes, level: int):
+    """Translation-stencil segments (bookmark, ranks, i16 offset codes)
+    (_ckernels.pyx:205-287)."""
+    return _segments("fmmb_stencil_segments", recv_boxes, src_boxes, level, True)
+
+
+# ------------------------------------------------------ directory helpers
+def propagate_to_parents(boxes):
+    """Ascending unique parents (lists.py:103-105)."""
+    dev = _host.pick_device(boxes)
+    dout = _host.is_device_input(boxes)
+    b = _dev_u64(boxes, dev)
+    out = torch.empty(max(b.numel(), 1), dtype=torch.uint64, device=dev)
+    cnt = C.c_int64(0)
+    _call("fmmb_propagate_to_parents", dev, _ptr(b), b.numel(), _ptr(out), C.byref(cnt))
+    return _out(out[: int(cnt.value)], dout)
+
+
+def exclusive_scan(values):
+    """(exclusive prefix sums, total) of non-negative integers (scan.py:25-73)."""
+    dev = _host.pick_device(values)
+    dout = _host.is_device_input(values)
+    v = _host.to_device(values, dev, torch.int64, (-1,))
+    if v.numel() == 0:
+        raise DomainError("scan input must be a non-empty 1-d array")
+    out = torch.empty_like(v)
+    tot = C.c_int64(0)
+    _call("fmmb_exclusive_scan_i64", dev, _ptr(v), v.numel(), _ptr(out), C.byref(tot))
+    return _out(out, dout), int(tot.value)
+
+
+def build_bookmarks(bins):
+    """(bookmarks, non-empty box indices) from a dense histogram
+    (pseudosort.py:68-78)."""
+    dev = _host.pick_device(bins)
+    dout = _host.is_device_input(bins)
+    b = _host.to_device(bins, dev, torch.int64, (-1,))
+    if b.numel() == 0:
+        z = torch.zeros(1, dtype=torch.int64, device=dev)
+        return _out(z, dout), _out(torch.empty(0, dtype=torch.uint64, device=dev), dout)
+    starts, total = exclusive_scan(b)
+    nz = torch.nonzero(b > 0).reshape(-1)
+    bm = torch.empty(nz.numel() + 1, dtype=torch.int64, device=dev)
+    bm[0] = 0
+    bm[1:] = starts[nz] + b[nz]
+    return _out(bm, dout), _out(nz.to(torch.int64).view(torch.uint64), dout)
+
+
+def reorder(points, charges, bins, boxes, ranks, max_level: int):
+    """Box-grouped copy from a (bins, boxes, ranks) sort index (pseudosort.py:105-135)."""
+    from .pseudosort import SortedPointSet
+
+    dev = _host.pick_device(points, charges, bins, boxes, ranks)
+    dout = _host.is_device_input(points, charges, bins, boxes, ranks)
+    pts = _host.points_to_device(points, dev)
+    n = pts.shape[0]
+    bx = _dev_u64(boxes, dev)
+    rk = _host.to_device(ranks, dev, torch.int64, (-1,))
+    if bx.numel() != n or rk.numel() != n:
+        raise DomainError("points and sort index lengths disagree")
+    bn = _host.to_device(bins, dev, torch.int64, (-1,))
+    starts, _ = exclusive_scan(bn)
+    positions = starts[bx.view(torch.int64)] + rk
+    perm = torch.empty(n, dtype=torch.int64, device=dev)
+    perm[positions] = torch.arange(n, dtype=torch.int64, device=dev)
+    bm, nz = build_bookmarks(bn)
+    q = None
+    if charges is not None:
+        q = _host.to_device(charges, dev, torch.float64, (-1,))[perm]
+    res = SortedPointSet(level=max_level, points=pts[perm], charges=q, permutation=perm,
+                         bookmarks=bm if isinstance(bm, torch.Tensor) else torch.from_numpy(bm),
+                         non_empty_index=nz if isinstance(nz, torch.Tensor) else torch.from_numpy(nz),
+                         boxes=bx[perm])
+    return res if dout else res.to_numpy()
+
+
+# ------------------------------------------------- evaluation (not the path)
+def near_field(*args, **kwargs):
+    raise NotImplementedError("near_field is outside the build path (SURVEY §8(f) row 1)")
+
+
+def direct_potentials(*args, **kwargs):
+    raise NotImplementedError("direct_potentials is outside the build path (SURVEY §8(f) row 1)")
+
+
+def install(fmmkit_module=None):
+    """Bind this module as the reference's kernel plugin
+    (`fmmkit.backend.kernels = kernels`, the swap of cli.py:263-266)."""
+    import sys
+
+    if fmmkit_module is None:
+        import fmmkit as fmmkit_module  # noqa: F811 - the caller's reference
+    fmmkit_module.backend.kernels = sys.modules[__name__]
+    return sys.modules[__name__]

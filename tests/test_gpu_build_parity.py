@@ -1,0 +1,62 @@
+"""build_all on the GPU vs the reference CPU build_all: every output array
+bit-identical (values, dtypes, shapes) on the same inputs."""
+
+import numpy as np
+import pytest
+
+from paper_1301_1704_b200.workloads import generate
+from tests.parity import compare_structures
+
+pytestmark = pytest.mark.gpu
+
+CASES = [
+    # (n_src, n_recv, level, dist, seed)
+    (3000, 3000, 4, "uniform", 60),
+    (4096, 4096, 5, "sphere", 27),
+    (2**16, 2**16, 4, "uniform", 1),  # c1
+    (1000, 700, 3, "uniform", 5),
+    (1, 1, 3, "uniform", 9),
+    (500, 0, 3, "uniform", 3),
+    (0, 400, 3, "uniform", 4),
+    (0, 0, 3, "uniform", 4),
+    (300, 200, 0, "uniform", 7),
+    (300, 200, 1, "uniform", 7),
+    (300, 200, 2, "uniform", 7),
+    (20000, 15000, 6, "sphere", 11),
+    (2**18, 2**18, 7, "uniform", 2),
+    (2**17, 2**17, 9, "sphere", 3),
+    (5000, 5000, 10, "sphere", 8),
+    (3000, 2000, 11, "uniform", 12),
+]
+
+
+@pytest.mark.parametrize("n,m,level,dist,seed", CASES)
+def test_build_all_matches_reference(gpu, ref, n, m, level, dist, seed):
+    src, q, _ = generate(n, 1, dist, seed)
+    _, _, recv = generate(1, m, dist, seed + 1000)
+    budget = max(2 << 30, 8 ** level * 8)
+    want = ref.build_all(src, q, recv, max_level=level, histogram_budget_bytes=budget)
+    got = gpu.build_all(src, q, recv, max_level=level, histogram_budget_bytes=budget)
+    errors = compare_structures(got, want)
+    assert not errors, "\n".join(errors)
+
+
+def test_build_all_receivers_without_charges(gpu, ref):
+    src, _, recv = generate(2000, 2000, "uniform", 13)
+    want = ref.build_all(src, None, recv, max_level=4)
+    got = gpu.build_all(src, None, recv, max_level=4)
+    assert got.sorted_src.charges is None
+    assert not compare_structures(got, want)
+
+
+def test_boundary_coordinates(gpu, ref):
+    one = 1.0
+    below = np.nextafter(1.0, 0.0)
+    pts = np.array([
+        [0.0, 0.0, 0.0], [one, one, one], [below, below, below], [2.0**-30, 0.5, one],
+        [0.5, 0.25, 0.75], [one, 0.0, below], [-0.0, 0.3, 0.3], [0.999999, 1e-300, 0.5],
+    ])
+    for level in (0, 1, 3, 7, 9):
+        want = ref.build_all(pts, np.arange(8.0), pts[::-1].copy(), max_level=level)
+        got = gpu.build_all(pts, np.arange(8.0), pts[::-1].copy(), max_level=level)
+        assert not compare_structures(got, want), level
