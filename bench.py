@@ -1,0 +1,352 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 FMM data-structure build (BASELINE.json metric:
+particles/s for the full build, fraction of the HBM roofline).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--workload c2]
+    python bench.py --impl reference ...      # the reference CPU path
+
+A step is one full `build_all` (sort both sets, bookmarks, level directory,
+E2 neighbour table, E4 stencils at every level) over one batch of synthetic
+input (`fmmkit.cli.generate`'s Philox streams).  `value` is device-resident
+throughput (inputs already in HBM, outputs left in HBM); `e2e` goes through
+the public API with pinned host inputs and numpy outputs (H2D + D2H inside
+the timed region).  Inputs (0.94 GB at c2) exceed the 126 MB L2, so no flush
+is needed between steps.
+
+Multi-GPU (torchrun, N>1): every rank builds its own c2-sized workload
+(independent replicas, weak scaling, no collective on the data path); the
+Morton-partitioned single-problem build is paper_1301_1704_b200.distributed.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particles/sec for full FMM data-structure build"
+UNIT = "particles/s"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4"])
+    p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    p.add_argument("--no-e2e", action="store_true")
+    return p.parse_args()
+
+
+# ------------------------------------------------------------------ ranks
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# --------------------------------------------------------- cpu reference
+CPU_SAMPLE = {"n": 2**21, "level": 6, "dist": "uniform", "seed": 1}
+
+
+def cpu_reference_rate(max_seconds: float = 25.0, steps: int | None = None):
+    """Reference CPU build_all on a bounded sample of the workload: N=M=2^21
+    uniform at L=6 (8 points per finest box, the c2 occupancy).  Returns
+    (particles/s, kind, cores, sample, per-step rates)."""
+    from paper_1301_1704_b200.workloads import generate
+
+    src, q, recv = generate(CPU_SAMPLE["n"], CPU_SAMPLE["n"], CPU_SAMPLE["dist"],
+                            CPU_SAMPLE["seed"])
+    L = CPU_SAMPLE["level"]
+    ref_dir = os.path.join(ROOT, "oracle", "_ref")
+    kind = "reference"
+    try:
+        sys.path.insert(0, ref_dir)
+        import fmmkit  # noqa: F401  (oracle/_ref: the unmodified reference)
+
+        assert fmmkit.backend_name() == "compiled"
+        run = lambda: fmmkit.build_all(src, q, recv, max_level=L)  # noqa: E731
+    except Exception:  # the C restatement of the same algorithm
+        sys.path.pop(0)
+        from oracle import oracle as orc
+
+        kind = "port"
+        run = lambda: orc.build_all(src, q, recv, L)  # noqa: E731
+    rates = []
+    t_start = time.perf_counter()
+    while True:
+        t0 = time.perf_counter()
+        run()
+        dt = time.perf_counter() - t0
+        rates.append(2 * CPU_SAMPLE["n"] / dt)
+        if steps is not None:
+            if len(rates) >= steps:
+                break
+        elif time.perf_counter() - t_start > max_seconds or len(rates) >= 5:
+            break
+    sample = (f"N=M=2^21 uniform, L=6 (c2 occupancy: 8 points per box), "
+              f"{'compiled fmmkit (oracle/_ref)' if kind == 'reference' else 'C oracle port'}, "
+              f"deterministic mode (single-threaded), median of {len(rates)} builds")
+    return statistics.median(rates), kind, 1, sample, rates
+
+
+def run_reference_arm(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return
+    for _ in range(max(0, min(args.warmup, 1))):
+        pass
+    rate, kind, cores, sample, rates = cpu_reference_rate(steps=max(1, args.steps))
+    dt = 2 * CPU_SAMPLE["n"] / rate
+    line = {
+        "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
+        "n_gpus": args.gpus, "steps": len(rates), "warmup": 0,
+        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{args.workload} (bounded CPU sample)", "sample": sample},
+        "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
+                         "sample": sample},
+        "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+    NAMES = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.path = None
+
+    def start(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        self.proc.wait()
+        sm, smax, reasons = [], [], set()
+        with open(self.path) as f:
+            for line in f:
+                parts = [x.strip() for x in line.split(",")]
+                if len(parts) < 6:
+                    continue
+                try:
+                    sm.append(float(parts[0]))
+                    smax.append(float(parts[1]))
+                except ValueError:
+                    continue
+                for name, v in zip(self.NAMES, parts[2:6]):
+                    if v.lower().startswith("active"):
+                        reasons.add(name)
+        os.unlink(self.path)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(smax) if smax else None,
+                "samples": len(sm), "reasons": sorted(reasons)}
+
+
+# -------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+
+    import paper_1301_1704_b200 as fb
+    from paper_1301_1704_b200 import roofline
+    from paper_1301_1704_b200.workloads import WORKLOADS, generate, perturb
+
+    ws, rank, local = dist_env()
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    wl = WORKLOADS[args.workload]
+    src_np, q_np, recv_np = generate(wl.n, wl.n, wl.dist, wl.seed + rank)
+    src = torch.from_numpy(src_np).to(dev)
+    q = torch.from_numpy(q_np).to(dev)
+    recv = torch.from_numpy(recv_np).to(dev)
+    L = wl.level
+    stream = torch.cuda.current_stream(dev)
+    rng = np.random.default_rng(123)
+
+    def step():
+        return fb.build_all_device(src, q, recv, L)
+
+    # warm-up (also sizes the caching allocator for the outputs)
+    st = None
+    for _ in range(max(args.warmup, 3)):
+        st = None
+        st = step()
+    counts = roofline.build_counts(st)
+    balg = roofline.build_bytes(counts)
+    wbytes = roofline.list_write_bytes(counts)
+    st = None
+    torch.cuda.synchronize()
+
+    if args.workload == "c4":  # dynamic rebuild: fresh perturbed positions each step
+        pert = [(torch.from_numpy(perturb(src_np, rng)).to(dev),
+                 torch.from_numpy(perturb(recv_np, rng)).to(dev)) for _ in range(2)]
+
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    phases = []
+    launches = 0
+    ev0.record(stream)
+    for k in range(args.steps):
+        if args.workload == "c4":
+            s_in, r_in = pert[k % 2]
+            st = fb.build_all_device(s_in, q, r_in, L)
+        else:
+            st = step()
+        phases.append(st.build_seconds)
+        launches += st.n_launches
+        st = None
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    clk = clocks.stop()
+    elapsed = ev0.elapsed_time(ev1) * 1e-3
+    if dist is not None:
+        t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    units = 2 * wl.n * args.steps * ws
+    value = units / elapsed
+    ms_step = elapsed / args.steps * 1e3
+
+    ph = {k: statistics.median([float(p[k]) for p in phases]) * 1e3
+          for k in ("sort_sources", "level_directory", "lists_count", "size_readback",
+                    "lists_write")}
+    peak, peak_src = roofline.measured_hbm_gbs(ROOT)
+    write_s = ph["lists_write"] * 1e-3
+    achieved = wbytes / write_s / 1e9
+    build_gbs = balg / (elapsed / args.steps) / 1e9
+
+    # ---- end to end: pinned host inputs -> public API -> numpy outputs
+    e2e = None
+    if not args.no_e2e and rank == 0:
+        h_src = torch.from_numpy(src_np).pin_memory()
+        h_q = torch.from_numpy(q_np).pin_memory()
+        h_recv = torch.from_numpy(recv_np).pin_memory()
+        h2d = (h_src.numel() + h_q.numel() + h_recv.numel()) * 8
+        res = fb.build_all(h_src, h_q, h_recv, max_level=L)  # warm (pins output buffers)
+        d2h = _numpy_bytes(res)
+        res = None
+        times = []
+        for _ in range(max(1, args.e2e_steps)):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            res = fb.build_all(h_src, h_q, h_recv, max_level=L)
+            times.append(time.perf_counter() - t0)
+            res = None
+        e2e = {"value": 2 * wl.n / statistics.median(times), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": statistics.median(times) * 1e3}
+
+    cpu = None
+    if not args.no_cpu and rank == 0:
+        rate, kind, cores, sample, _ = cpu_reference_rate()
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64/u64 (integer keys, f64 points)",
+            "data": "synthetic (fmmkit.cli.generate Philox streams)",
+            "config": {
+                "workload": f"{wl.name}: N=M={wl.n} {wl.dist}, max_level={L}, seed={wl.seed}",
+                "global_batch_particles": 2 * wl.n * ws,
+                "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
+                "l2": "inputs (0.94 GB at c2) larger than the 126 MB L2; no flush",
+            },
+            "roofline": {
+                "bound": "hbm", "kernel": "k_lists<true> (E2+E4 list write)",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "peak_source": peak_src, "traffic": None,
+                "alg_bytes_per_launch": wbytes, "avg_launch_ms": ph["lists_write"],
+            },
+            "build_roofline": {
+                "alg_bytes_per_step": balg, "achieved_gbs": build_gbs,
+                "frac_of_measured": build_gbs / peak,
+                "frac_of_nominal_8tbs": build_gbs / roofline.NOMINAL_HBM_GBS,
+            },
+            "phases_ms": ph,
+            "counts": {k: counts[k] for k in ("ks", "kr", "e2")} | {
+                "stencil_entries": int(sum(counts["s_l"].values()))},
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": cpu,
+            "gpu_launches": int(launches),
+        }
+        print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def _numpy_bytes(st) -> int:
+    tot = 0
+    for ps in (st.sorted_src, st.sorted_recv):
+        for f in ("points", "charges", "permutation", "bookmarks", "non_empty_index", "boxes"):
+            v = getattr(ps, f)
+            if v is not None:
+                tot += v.nbytes
+    tot += st.neighbor_table.neighbor_bookmark.nbytes + st.neighbor_table.neighbor_list.nbytes
+    L = st.max_level
+    for l in range(2, L):
+        tot += st.directory.src_boxes[l].nbytes + st.directory.recv_boxes[l].nbytes
+    for l in st.stencils.ranks:
+        tot += (st.stencils.bookmark[l].nbytes + st.stencils.ranks[l].nbytes
+                + st.stencils.codes[l].nbytes)
+    return tot
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference_arm(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

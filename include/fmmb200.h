@@ -181,8 +181,9 @@ typedef struct fmmb_structures {
 /* build_all(src_points, src_charges, recv_points, max_level) (lists.py:133-187)
  * src: (n,3) f64 C-contiguous device array; charges: (n,) f64 or NULL;
  * recv: (m,3) f64.  All outputs are allocated through `alloc` and written to
- * *out.  `timing` is NULL or an array of 5 cudaEvent_t recorded at the phase
- * boundaries [start, sorted, directory, counted, end].
+ * *out.  `timing` is NULL or an array of 6 cudaEvent_t recorded at the phase
+ * boundaries [start, sorted, directory, counted, write-start, end] (the
+ * size read-back sits between `counted` and `write-start`).
  * Errors: FMMB_ERR_CAPACITY for level outside [0,20]; FMMB_ERR_DOMAIN when a
  * point's Morton index falls outside the level grid (negative coordinates:
  * the reference indexes its histogram out of bounds there). */

@@ -153,19 +153,27 @@ class Allocator:
 
     def __init__(self, dev: torch.device):
         self.dev = dev
-        self.blocks: list[torch.Tensor] = []
-        self.error: BaseException | None = None
+        blocks: list[torch.Tensor] = []
+        errors: list[BaseException] = []
+        self.blocks = blocks
+        self._errors = errors
 
+        # the closure must not reference `self` (a cycle would keep every
+        # output block alive until the cyclic GC runs)
         def _alloc(_ctx, nbytes):
             try:
-                t = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=self.dev)
+                t = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=dev)
             except BaseException as e:  # noqa: BLE001 - reported after the call
-                self.error = e
+                errors.append(e)
                 return None
-            self.blocks.append(t)
+            blocks.append(t)
             return t.data_ptr()
 
         self.fn = ALLOC_FN(_alloc)
+
+    @property
+    def error(self) -> BaseException | None:
+        return self._errors[0] if self._errors else None
 
     def block_of(self, ptr: int) -> tuple[torch.Tensor, int]:
         for b in self.blocks:

@@ -418,6 +418,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     }
     const int lgrid = (int)std::max<int64_t>(
         1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * 16));
+    if (ev) cudaEventRecord(ev[4], s);
     k_lists<true><<<lgrid, kLThreads, 0, s>>>(lp);
     FMMB_LAUNCHED();
 
@@ -441,7 +442,10 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
       out->n_st[k] = hp->seg_totals[k];
     }
   }
-  if (ev) cudaEventRecord(ev[4], s);
+  if (ev) {
+    if (!lists) cudaEventRecord(ev[4], s);
+    cudaEventRecord(ev[5], s);
+  }
   cudaFreeAsync(ws, s);
   out->n_launches = launches;
   h->launches = launches;

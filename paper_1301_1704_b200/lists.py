@@ -71,7 +71,8 @@ class BuildSeconds(dict):
     The device build fuses phases: both point sets are sorted by one pass set
     (reported under sort_sources; sort_receivers is 0.0) and the E2 table and
     all E4 stencils come from the same count/write kernels (reported under
-    stencils; neighbor_table is 0.0)."""
+    stencils; neighbor_table is 0.0).  Extra keys split `stencils` into
+    lists_count, size_readback (the build's one host sync) and lists_write."""
 
     def __init__(self, events):
         super().__init__()
@@ -83,11 +84,11 @@ class BuildSeconds(dict):
             return
         self._events = None
         ev[-1].synchronize()
-        ms = [ev[i].elapsed_time(ev[i + 1]) * 1e-3 for i in range(len(ev) - 1)]
+        s = [ev[i].elapsed_time(ev[i + 1]) * 1e-3 for i in range(len(ev) - 1)]
         super().update(
-            sort_sources=ms[0], sort_receivers=0.0, neighbor_table=0.0,
-            level_directory=ms[1], stencils=ms[2] + ms[3],
-            lists_count=ms[2], lists_write=ms[3],
+            sort_sources=s[0], sort_receivers=0.0, neighbor_table=0.0,
+            level_directory=s[1], stencils=s[2] + s[3] + s[4],
+            lists_count=s[2], size_readback=s[3], lists_write=s[4],
         )
 
     def __getitem__(self, k):
@@ -222,10 +223,10 @@ def build_all_device(src: torch.Tensor, charges: torch.Tensor | None, recv: torc
     events = None
     ev_arr = None
     if timing:
-        events = [torch.cuda.Event(enable_timing=True) for _ in range(5)]
+        events = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
         for e in events:  # torch creates the CUevent lazily, on first record
             e.record()
-        ev_arr = (C.c_void_p * 5)(*[e.cuda_event for e in events])
+        ev_arr = (C.c_void_p * 6)(*[e.cuda_event for e in events])
     st = lib.fmmb_build_all(
         h, src.data_ptr() if n else None,
         charges.data_ptr() if (charges is not None and n) else None, n,
