@@ -251,7 +251,7 @@ def reorder(points, charges, bins, boxes, ranks, max_level: int):
     res = SortedPointSet(level=max_level, points=pts[perm], charges=q, permutation=perm,
                          bookmarks=bm if isinstance(bm, torch.Tensor) else torch.from_numpy(bm),
                          non_empty_index=nz if isinstance(nz, torch.Tensor) else torch.from_numpy(nz),
-                         boxes=bx[perm])
+                         boxes=bx.view(torch.int64)[perm].view(torch.uint64))
     return res if dout else res.to_numpy()
 
 

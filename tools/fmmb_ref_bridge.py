@@ -1,0 +1,43 @@
+"""pytest plugin: run the REFERENCE's own test-suite against this framework.
+
+Loaded with `-p fmmb_ref_bridge` before collection: binds the B200 kernel
+plugin as `fmmkit.backend.kernels` (the reference's own swap mechanism,
+cli.py:263-266) and replaces the build API entry points the tests import
+(`from fmmkit import build_all, sort_points, ...`) with the device versions.
+Test infrastructure only.
+"""
+
+import fmmkit
+import fmmkit.backend as _backend
+import fmmkit.lists as _lists
+import fmmkit.pseudosort as _pseudosort
+
+import paper_1301_1704_b200 as fb
+from paper_1301_1704_b200 import kernels as _kernels
+
+_backend.kernels = _kernels
+for _name in ("build_all", "sort_points", "histogram_and_sort_index", "reorder",
+              "build_bookmarks", "build_neighbor_table", "build_level_directory",
+              "build_translation_stencils", "propagate_to_parents", "choose_max_level"):
+    _obj = getattr(fb, _name)
+    setattr(fmmkit, _name, _obj)
+    for _mod in (_lists, _pseudosort):
+        if hasattr(_mod, _name):
+            setattr(_mod, _name, _obj)
+
+CALLS = {"build_all": 0}
+_orig_build_all = fb.build_all
+
+
+def _counting_build_all(*a, **k):
+    CALLS["build_all"] += 1
+    return _orig_build_all(*a, **k)
+
+
+fmmkit.build_all = _counting_build_all
+_lists.build_all = _counting_build_all
+
+
+def pytest_terminal_summary(terminalreporter):
+    terminalreporter.write_line(f"fmmb_ref_bridge: build_all calls routed to the B200 build: "
+                                f"{CALLS['build_all']}")
