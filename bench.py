@@ -300,7 +300,7 @@ def run_ours(args):
                 "l2": "inputs (0.94 GB at c2) larger than the 126 MB L2; no flush",
             },
             "roofline": {
-                "bound": "hbm", "kernel": "k_lists<true> (E2+E4 list write)",
+                "bound": "hbm", "kernel": "k_lists_write (E2+E4 list write)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_source": peak_src, "traffic": None,
                 "alg_bytes_per_launch": wbytes, "avg_launch_ms": ph["lists_write"],

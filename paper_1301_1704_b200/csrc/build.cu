@@ -201,6 +201,8 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
   const size_t o_va = z.take<uint32_t>(tot), o_vb = z.take<uint32_t>(tot);
   const size_t o_lowkeys = z.take<uint64_t>(2 * (1 + 8));  // levels 0,1 keys
   const size_t o_cnt = z.take<uint32_t>(cnt_cap);
+  const size_t o_lay = z.take<ListsLayout>(1);
+
   char* ws = nullptr;
   if (cudaMallocAsync((void**)&ws, z.off, s) != cudaSuccess)
     return fmmb_fail(h, FMMB_ERR_CUDA, "workspace allocation of %zu bytes failed", z.off);
@@ -345,10 +347,13 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     if (L == 0) nwork_cap = 1;
     const int lgrid = (int)std::max<int64_t>(
         1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * 16));
-    k_lists<false><<<lgrid, kLThreads, 0, s>>>(lp);
+    ListsLayout* glay = (ListsLayout*)W(o_lay);
+    k_lists_plan<<<1, 32, 0, s>>>(lp, glay);
+    FMMB_LAUNCHED();
+    k_lists_count<<<lgrid, kLThreads, 0, s>>>(lp, glay);
     FMMB_LAUNCHED();
     k_lists_scan<<<(unsigned)std::max<int64_t>(1, scan_tiles_cap), kScanThreads, 0, s>>>(
-        lp, (uint64_t*)W(o_lst), tc + 10, dplan->seg_totals);
+        lp, glay, (uint64_t*)W(o_lst), tc + 10, dplan->seg_totals);
     FMMB_LAUNCHED();
   }
   if (ev) cudaEventRecord(ev[3], s);
@@ -419,7 +424,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     const int lgrid = (int)std::max<int64_t>(
         1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * 16));
     if (ev) cudaEventRecord(ev[4], s);
-    k_lists<true><<<lgrid, kLThreads, 0, s>>>(lp);
+    k_lists_write<<<lgrid, kLThreads, 0, s>>>(lp, (const ListsLayout*)W(o_lay));
     FMMB_LAUNCHED();
 
     out->neighbor_bookmark = lp.bm[0];
