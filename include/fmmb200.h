@@ -68,6 +68,14 @@ FMMB_API fmmb_status fmmb_destroy(fmmb_handle_t h);
 FMMB_API const char* fmmb_last_error(fmmb_handle_t h);
 /* number of kernel launches issued by the last call on this handle */
 FMMB_API int64_t fmmb_last_launch_count(fmmb_handle_t h);
+/* Sort-phase strategy of fmmb_build_all / fmmb_sort_points (no reference
+ * counterpart; both strategies give bit-identical outputs):
+ *   0 = auto: payload-carrying bucket sort, rerun on the Onesweep path if a
+ *       bucket overflows the bucket sort's shared-memory capacity;
+ *   1 = bucket sort (with the same overflow rerun);  2 = Onesweep LSD + gather.
+ * fmmb_last_sort_path() reports the path the last build completed on (1/2). */
+FMMB_API fmmb_status fmmb_set_sort_path(fmmb_handle_t h, int path);
+FMMB_API int fmmb_last_sort_path(fmmb_handle_t h);
 
 /* ------------------------------------------------------ kernel plugin level */
 

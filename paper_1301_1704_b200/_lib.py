@@ -57,6 +57,8 @@ SIGNATURES = [
     ("fmmb_destroy", C.c_int, [_p]),
     ("fmmb_last_error", C.c_char_p, [_p]),
     ("fmmb_last_launch_count", _i64, [_p]),
+    ("fmmb_set_sort_path", C.c_int, [_p, C.c_int]),
+    ("fmmb_last_sort_path", C.c_int, [_p]),
     ("fmmb_spread_bits", C.c_int, [_p, _p, _i64, _p, _p]),
     ("fmmb_compact_bits", C.c_int, [_p, _p, _i64, _p, _p]),
     ("fmmb_interleave_coords", C.c_int, [_p, _p, _p, _p, _i64, _p, _p]),
@@ -128,6 +130,22 @@ def handle(dev: torch.device) -> int:
         h = out.value
         _handles[idx] = h
     return h
+
+
+SORT_PATHS = {1: "bucket", 2: "onesweep"}
+_SORT_PATH_IDS = {"auto": 0, "bucket": 1, "onesweep": 2}
+
+
+def set_sort_path(path: str, device=None) -> None:
+    """Select the sort-phase strategy of the fused build on a device:
+    "auto" (bucket sort, Onesweep rerun on overflow), "bucket" or "onesweep".
+    Both strategies produce bit-identical outputs."""
+    if path not in _SORT_PATH_IDS:
+        raise ValueError(f"unknown sort path {path!r}")
+    dev = device_of(device)
+    h = handle(dev)
+    st = load().fmmb_set_sort_path(h, _SORT_PATH_IDS[path])
+    check(st, h)
 
 
 def stream_of(dev: torch.device) -> int:

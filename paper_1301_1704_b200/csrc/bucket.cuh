@@ -1,0 +1,854 @@
+// Sort side of the build, payload-carrying bucket sort (the fast path).
+//
+// Reference semantics reproduced: pseudosort.histogram_and_sort_index +
+// reorder + build_bookmarks (pseudosort.py:41-135), i.e. the permutation is
+// np.argsort(keys, kind="stable") (tests/test_pseudosort.py:94-104) with the
+// compiled backend's encode (_ckernels.pyx:85-104).  A bucket is a contiguous
+// range of Morton keys (the top `bb` key bits of one set), so the sorted
+// buckets concatenated are the global order and no box straddles two buckets.
+//
+//   H  k_bkt_hist    : read xyz once; per-CTA histogram of the bucket ids in
+//                      shared memory, one row per CTA.
+//   S  k_bkt_scan    : column sums, exclusive scan -> bucket starts; the
+//                      starts seed one global cursor per bucket.
+//   S  k_bkt_scatter : read xyz(+q) again; each warp owns a contiguous input
+//                      RANGE and moves its points, as 32-byte records
+//                      {x, y, z, q | recv index}, to its buckets' cursors
+//                      (warp-aggregated atomics).  Cursors advance in time, so
+//                      every bucket fills front to back and L2 merges the
+//                      partial lines; the order inside a bucket is by range
+//                      chunk, not by input index.
+//   L  k_bkt_local   : one CTA per bucket: TMA bulk copy of the bucket's
+//                      records into shared memory, stable LSD sort of the
+//                      composite (low key bits, range id) -- the range id
+//                      restores input order, since a range's chunks land in
+//                      its input order -- then the reference layout (points,
+//                      charges, permutation, boxes) with box heads giving the
+//                      bookmarks, non-empty keys and level-L occupancy bits.
+//
+// DRAM bytes per point (src / recv): H 24/24, S 32+36 / 24+32, L 36+48 / 32+40.
+//
+// The fast path needs every bucket to fit the local sort's shared memory
+// (kLcCap points); buckets hold <= 1024 points on average by construction.
+// Skewed inputs (dense clusters) overflow it: the local kernel then raises
+// `fail` and the host reruns the sort phase on the general Onesweep path
+// (sort.cuh + finalize.cuh).
+#pragma once
+#include "common.cuh"
+
+namespace fmmb {
+
+constexpr int kBucketBitsMax = 14;  // <= 2^14 buckets per set
+constexpr int kBucketAvg = 1024;    // bb chosen so the mean bucket is <= this
+constexpr int kWidBitsMax = 11;     // <= 2048 scatter ranges
+constexpr int kHThreads = 512;      // H pass
+constexpr int kHItems = 8;          // rows per lane per step (memory-level parallelism)
+constexpr int kHChunk = 32 * kHItems;
+constexpr int kSItems = 4;          // S pass: rows per lane per step (double-buffered)
+constexpr int kSChunk = 32 * kSItems;
+constexpr int kScanBuckets = 1024;  // buckets per CTA of the scan
+constexpr int kCursorStride = 32;   // u32 words per bucket cursor: one 128-B line each, so
+                                    // the scatter's cursor atomics never share an L2 line
+
+struct BucketGeo {
+  int sbits;      // 3L
+  int bb;         // bucket bits per set
+  int shift;      // 3L - bb: low key bits sorted inside a bucket
+  int nb;         // 2 << bb buckets
+  int64_t n, m;   // sources, receivers
+  int rbits;      // input points per scatter range = 2^rbits (>= kSChunk)
+  int nranges;
+  int wbits;      // bits of a range id
+  int hgrid;      // CTAs (histogram rows) of the H pass
+  int swarps;     // warps per CTA of the S pass
+};
+
+__host__ inline int ceil_log2(int64_t v) {
+  int b = 0;
+  while (b < 62 && (1ll << b) < v) ++b;
+  return b;
+}
+
+__host__ inline BucketGeo bucket_geo(int level, int64_t n, int64_t m, int num_sms) {
+  BucketGeo g{};
+  g.sbits = 3 * level;
+  const int64_t nmax = n > m ? n : m;
+  int bb = ceil_log2((nmax + kBucketAvg - 1) / kBucketAvg);
+  if (bb > kBucketBitsMax) bb = kBucketBitsMax;
+  if (bb > g.sbits) bb = g.sbits;
+  g.bb = bb;
+  g.shift = g.sbits - bb;
+  g.nb = 2 << bb;
+  g.n = n;
+  g.m = m;
+  const int64_t tot = n + m;
+  int rb = ceil_log2((tot + (1 << kWidBitsMax) - 1) >> kWidBitsMax);
+  if ((1 << rb) < kSChunk) rb = ceil_log2(kSChunk);
+  g.rbits = rb;
+  g.nranges = (int)((tot + (1ll << rb) - 1) >> rb);
+  if (g.nranges < 1) g.nranges = 1;
+  g.wbits = ceil_log2(g.nranges);
+  g.swarps = (g.nranges + num_sms - 1) / num_sms;
+  if (g.swarps > 16) g.swarps = 16;
+  const int64_t hchunks = (tot + (int64_t)kHThreads * kHItems - 1) / ((int64_t)kHThreads * kHItems);
+  g.hgrid = (int)(hchunks < num_sms ? (hchunks < 1 ? 1 : hchunks) : num_sms);
+  return g;
+}
+
+// rows of the combined [src | recv] input: point i < n is src[i], else recv[i-n]
+__device__ __forceinline__ const double* row_ptr(const double* src, const double* recv,
+                                                 int64_t n, int64_t i) {
+  return i < n ? src + 3 * i : recv + 3 * (i - n);
+}
+
+__device__ __forceinline__ uint32_t bucket_of(uint64_t key, int is_recv, const BucketGeo& g) {
+  return ((uint32_t)is_recv << g.bb) | (uint32_t)(key >> g.shift);
+}
+
+// ---------------------------------------------------------------- H pass --
+template <bool NARROW>
+__global__ void __launch_bounds__(kHThreads)
+    k_bkt_hist(const double* __restrict__ src, const double* __restrict__ recv,
+               const BucketGeo g, int level, uint32_t* __restrict__ mat,
+               uint32_t* __restrict__ err) {
+  extern __shared__ uint32_t s_hist[];  // [nb]
+  const int lane = threadIdx.x & 31;
+  for (int b = threadIdx.x; b < g.nb; b += kHThreads) s_hist[b] = 0;
+  __syncthreads();
+  const int64_t tot = g.n + g.m;
+  const uint64_t lim = 1ull << g.sbits;
+  const double grid = (double)(1ll << level);
+  bool bad = false;
+  const int64_t wstride = (int64_t)g.hgrid * (kHThreads / 32);
+  for (int64_t c = (int64_t)blockIdx.x * (kHThreads / 32) + (threadIdx.x >> 5);
+       c * kHChunk < tot; c += wstride) {
+    const int64_t base = c * kHChunk;
+    double x[kHItems], y[kHItems], z[kHItems];
+#pragma unroll
+    for (int k = 0; k < kHItems; ++k) {
+      const int64_t i = base + k * 32 + lane;
+      if (i < tot) {
+        const double* p = row_ptr(src, recv, g.n, i);
+        x[k] = __ldg(p);
+        y[k] = __ldg(p + 1);
+        z[k] = __ldg(p + 2);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kHItems; ++k) {
+      const int64_t i = base + k * 32 + lane;
+      if (i < tot) {
+        const uint64_t key = encode_any<NARROW>(x[k], y[k], z[k], level, grid);
+        bad |= key >= lim;
+        atomicAdd(&s_hist[bucket_of(key & (lim - 1), i >= g.n, g)], 1u);
+      }
+    }
+  }
+  if (__any_sync(0xffffffffu, bad) && lane == 0) atomicOr(err, 1u);
+  __syncthreads();
+  uint32_t* row = mat + (size_t)blockIdx.x * g.nb;
+  for (int b = threadIdx.x; b < g.nb; b += kHThreads) row[b] = s_hist[b];
+}
+
+// ------------------------------------------------------------- scan pass --
+// CTA = kScanBuckets buckets in order (ticket + decoupled look-back).
+// bstart[b] = first sorted position of bucket b (bstart[nb] = n + m),
+// cursor[b] = bstart[b], *maxb = largest bucket.
+__global__ void __launch_bounds__(256)
+    k_bkt_scan(const uint32_t* __restrict__ mat, const BucketGeo g, uint32_t* __restrict__ bstart,
+               uint32_t* __restrict__ cursor, uint64_t* __restrict__ states,
+               uint32_t* __restrict__ ticket, uint32_t* __restrict__ maxb) {
+  constexpr int kPer = kScanBuckets / 256;
+  __shared__ uint32_t s_w[8];
+  __shared__ int64_t s_tile, s_base;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int b0 = (int)tile * kScanBuckets + threadIdx.x * kPer;
+  uint32_t c[kPer];
+  uint32_t tsum = 0, tmax = 0;
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    c[e] = 0;
+    const int b = b0 + e;
+    if (b < g.nb)
+      for (int r = 0; r < g.hgrid; ++r) c[e] += __ldg(mat + (size_t)r * g.nb + b);
+    tsum += c[e];
+    tmax = c[e] > tmax ? c[e] : tmax;
+  }
+  tmax = __reduce_max_sync(0xffffffffu, tmax);
+  if (lane == 0 && tmax) atomicMax(maxb, tmax);
+  uint32_t wt;
+  uint32_t x = warp_excl_scan(tsum, wt);
+  if (lane == 0) s_w[warp] = wt;
+  __syncthreads();
+  uint32_t all = 0;
+  for (int i = 0; i < 8; ++i) {
+    x += i < warp ? s_w[i] : 0u;
+    all += s_w[i];
+  }
+  if (threadIdx.x == 0) {
+    uint64_t* st = states + tile;
+    uint64_t excl = 0;
+    if (tile == 0) {
+      st_state(st, kStInclusive | all);
+    } else {
+      st_state(st, kStAggregate | all);
+      excl = lookback(states, tile, 0, 1);
+      st_state(st, kStInclusive | (excl + all));
+    }
+    s_base = (int64_t)excl;
+    if ((int64_t)(tile + 1) * kScanBuckets >= g.nb) bstart[g.nb] = (uint32_t)(excl + all);
+  }
+  __syncthreads();
+  uint32_t run = (uint32_t)s_base + x;
+#pragma unroll
+  for (int e = 0; e < kPer; ++e) {
+    const int b = b0 + e;
+    if (b < g.nb) {
+      bstart[b] = run;
+      cursor[(size_t)b * kCursorStride] = run;
+    }
+    run += c[e];
+  }
+}
+
+// ---------------------------------------------------------- scatter pass --
+__device__ __forceinline__ void st_v4f64(double* p, double a, double b, double c, double d) {
+  asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
+               "d"(d)
+               : "memory");
+}
+
+// mbarrier / bulk-copy helpers (TMA 1-D bulk copies, sm_90+ / sm_100a)
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+          "r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// S pass.  Each warp streams its range in chunks of kSRows rows through a
+// kSStages-deep shared-memory ring filled by TMA bulk copies (one elected
+// lane; chunks that straddle the src/recv boundary, end the range early or
+// are not 16-byte aligned are loaded by the warp instead).  Chunk c+1's
+// cursor atomics are in flight while chunk c is stored, and chunks c+1, c+2
+// are in flight from HBM, so neither round trip is exposed.
+constexpr int kSRows = 128;
+constexpr int kSStages = 3;
+constexpr int kSStageBytes = kSRows * 32;  // xyz (24 B) + q (8 B) per row
+constexpr int kSMaxWarps = 16;
+
+__host__ inline size_t scatter_smem_bytes(int warps) {
+  return (size_t)warps * kSStages * (kSStageBytes + 8);
+}
+
+template <bool NARROW>
+__global__ void __launch_bounds__(kSMaxWarps * 32)
+    k_bkt_scatter(const double* __restrict__ src, const double* __restrict__ q,
+                  const double* __restrict__ recv, const BucketGeo g, int level,
+                  uint32_t* __restrict__ cursor, double* __restrict__ rec,
+                  uint32_t* __restrict__ idx) {
+  extern __shared__ __align__(128) unsigned char sc_smem[];
+  constexpr int kItems = kSRows / 32;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * g.swarps + warp;
+  if (r >= g.nranges) return;  // warp-uniform; no block barriers below
+  double* stage0 = reinterpret_cast<double*>(sc_smem) + (size_t)warp * kSStages * (kSStageBytes / 8);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sc_smem + (size_t)g.swarps * kSStages * kSStageBytes) +
+                   warp * kSStages;
+  if (lane == 0) {
+    for (int st = 0; st < kSStages; ++st) mbar_init(bars + st);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const int64_t n = g.n, tot = n + g.m;
+  const int64_t lo = (int64_t)r << g.rbits;
+  const int64_t hi = lo + (1ll << g.rbits) < tot ? lo + (1ll << g.rbits) : tot;
+  const int nchunks = (int)((hi - lo + kSRows - 1) / kSRows);
+  const uint64_t kmask = (1ull << g.sbits) - 1ull;
+  const double grid = (double)(1ll << level);
+  const unsigned lt = lanemask_lt();
+
+  auto issue = [&](int c) {  // fill stage c % kSStages with chunk c
+    const int st = c % kSStages;
+    double* xyz = stage0 + (size_t)st * (kSStageBytes / 8);
+    double* qs = xyz + 3 * kSRows;
+    const int64_t base = lo + (int64_t)c * kSRows;
+    const int rows = (int)(hi - base < kSRows ? hi - base : kSRows);
+    const bool is_src = base < n;
+    const double* rp = row_ptr(src, recv, n, base);
+    const bool tma = rows == kSRows && (base + kSRows <= n || base >= n) &&
+                     ((uintptr_t)rp & 15) == 0 &&
+                     (!is_src || !q || ((uintptr_t)(q + base) & 15) == 0);
+    __syncwarp();  // every lane is done reading this stage (chunk c - kSStages)
+    if (tma) {
+      if (lane == 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        const uint32_t qbytes = (is_src && q) ? kSRows * 8 : 0;
+        mbar_expect_tx(bars + st, kSRows * 24 + qbytes);
+        bulk_g2s(xyz, rp, kSRows * 24, bars + st);
+        if (qbytes) bulk_g2s(qs, q + base, qbytes, bars + st);
+      }
+    } else {
+      for (int k = 0; k < kItems; ++k) {
+        const int row = k * 32 + lane;
+        const int64_t i = base + row;
+        if (row < rows) {
+          const double* p = row_ptr(src, recv, n, i);
+          xyz[3 * row] = __ldg(p);
+          xyz[3 * row + 1] = __ldg(p + 1);
+          xyz[3 * row + 2] = __ldg(p + 2);
+          if (i < n) qs[row] = q ? __ldg(q + i) : 0.0;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bars + st);
+    }
+  };
+  auto wait = [&](int c) { mbar_wait(bars + c % kSStages, (uint32_t)(c / kSStages) & 1u); };
+  auto claim = [&](int c, unsigned (&pe)[kItems], uint32_t (&cu)[kItems]) {
+    const double* xyz = stage0 + (size_t)(c % kSStages) * (kSStageBytes / 8);
+    const int64_t base = lo + (int64_t)c * kSRows;
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const int row = k * 32 + lane;
+      const int64_t i = base + row;
+      uint32_t b = 0xFFFFFFFFu;
+      if (i < hi)
+        b = bucket_of(encode_any<NARROW>(xyz[3 * row], xyz[3 * row + 1], xyz[3 * row + 2],
+                                         level, grid) &
+                          kmask,
+                      i >= n, g);
+      pe[k] = __match_any_sync(0xffffffffu, b);
+      cu[k] = 0;
+      if (i < hi && lane == __ffs(pe[k]) - 1)
+        cu[k] = atomicAdd(cursor + (size_t)b * kCursorStride, __popc(pe[k]));
+    }
+  };
+  auto store = [&](int c, const unsigned (&pe)[kItems], const uint32_t (&cu)[kItems]) {
+    const double* xyz = stage0 + (size_t)(c % kSStages) * (kSStageBytes / 8);
+    const double* qs = xyz + 3 * kSRows;
+    const int64_t base = lo + (int64_t)c * kSRows;
+#pragma unroll
+    for (int k = 0; k < kItems; ++k) {
+      const int row = k * 32 + lane;
+      const int64_t i = base + row;
+      const uint32_t before = __shfl_sync(0xffffffffu, cu[k], __ffs(pe[k]) - 1);
+      if (i < hi) {
+        const uint32_t dst = before + __popc(pe[k] & lt);
+        const double w = i < n ? (q ? qs[row] : 0.0) : __longlong_as_double(i - n);
+        st_v4f64(rec + 4 * (size_t)dst, xyz[3 * row], xyz[3 * row + 1], xyz[3 * row + 2], w);
+        if (i < n) idx[dst] = (uint32_t)i;
+      }
+    }
+  };
+  unsigned pa[kItems], pb[kItems];
+  uint32_t ua[kItems], ub[kItems];
+  auto step = [&](int c, const unsigned (&pc)[kItems], const uint32_t (&uc)[kItems],
+                  unsigned (&pn)[kItems], uint32_t (&un)[kItems]) {
+    if (c + kSStages - 1 < nchunks) issue(c + kSStages - 1);
+    if (c + 1 < nchunks) {
+      wait(c + 1);
+      claim(c + 1, pn, un);
+    }
+    store(c, pc, uc);
+  };
+  for (int c = 0; c < kSStages - 1 && c < nchunks; ++c) issue(c);
+  wait(0);
+  claim(0, pa, ua);
+  for (int c = 0; c < nchunks; c += 2) {  // unrolled by two: static register buffers
+    step(c, pa, ua, pb, ub);
+    if (c + 1 < nchunks) step(c + 1, pb, ub, pa, ua);
+  }
+}
+
+// ------------------------------------------------------------ local pass --
+constexpr int kLcWarps = 8;
+constexpr int kLcThreads = kLcWarps * 32;
+constexpr int kLcDigit = 8;  // digit bits per in-smem LSD pass (fallback path)
+constexpr int kLcBins = 1 << kLcDigit;
+constexpr int kLcCap = 1280;  // points per bucket held in shared memory
+constexpr int kLcSmallBits = 11;  // box-count path: <= 2^11 boxes per bucket
+static_assert((1 << kLcSmallBits) <= kLcWarps * kLcBins, "box counters share s_wh");
+
+template <typename CK>
+__host__ __device__ constexpr size_t lc_smem_bytes() {
+  // records | idx | composite x2 | slot x2 | per-warp digit counters | misc
+  return (size_t)kLcCap * (32 + 4 + 2 * sizeof(CK) + 2 * 2) +
+         (size_t)kLcWarps * kLcBins * 4 + 128;
+}
+
+// One stable counting pass over digit [ds, ds+db) of B keys: warps own
+// contiguous slices (ordered); per-warp digit counts by shared atomics, a
+// digit-major scan over (digit, warp), then the placement walk ranks lanes
+// with match.any so equal digits keep their order.
+template <typename CK>
+__device__ __forceinline__ void lc_pass(const CK* kin, const uint16_t* pin, CK* kout,
+                                        uint16_t* pout, int B, int ds, int db,
+                                        uint32_t* s_wh, uint32_t* s_red) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nbins = 1 << db;
+  const uint32_t dm = (uint32_t)nbins - 1u;
+  const int slice = ((B + kLcThreads - 1) / kLcThreads) * 32;
+  const int lo = warp * slice;
+  const int hi = lo + slice < B ? lo + slice : B;
+  uint32_t* wh = s_wh + warp * kLcBins;
+  for (int d = lane; d < nbins; d += 32) wh[d] = 0;
+  __syncwarp();
+  for (int j = lo + lane; j < hi; j += 32) atomicAdd(&wh[(uint32_t)(kin[j] >> ds) & dm], 1u);
+  __syncthreads();
+  // digit-major exclusive offsets: thread t owns digits [t*dpt, (t+1)*dpt)
+  constexpr int dpt = (kLcBins + kLcThreads - 1) / kLcThreads;
+  uint32_t tsum = 0;
+#pragma unroll
+  for (int e = 0; e < dpt; ++e) {
+    const int d = threadIdx.x * dpt + e;
+    if (d < nbins)
+#pragma unroll
+      for (int w = 0; w < kLcWarps; ++w) tsum += s_wh[w * kLcBins + d];
+  }
+  uint32_t wt;
+  uint32_t x = warp_excl_scan(tsum, wt);
+  if (lane == 0) s_red[warp] = wt;
+  __syncthreads();
+  for (int i = 0; i < warp; ++i) x += s_red[i];
+#pragma unroll
+  for (int e = 0; e < dpt; ++e) {
+    const int d = threadIdx.x * dpt + e;
+    if (d < nbins)
+#pragma unroll
+      for (int w = 0; w < kLcWarps; ++w) {
+        const uint32_t c = s_wh[w * kLcBins + d];
+        s_wh[w * kLcBins + d] = x;
+        x += c;
+      }
+  }
+  __syncthreads();
+  const unsigned lt = lanemask_lt();
+  for (int j0 = lo; j0 < hi; j0 += 32) {
+    const int j = j0 + lane;
+    CK k = 0;
+    uint32_t d = 0xFFFFFFFFu;
+    if (j < hi) {
+      k = kin[j];
+      d = (uint32_t)(k >> ds) & dm;
+    }
+    const unsigned peers = __match_any_sync(0xffffffffu, d);
+    const int leader = 31 - __clz(peers);  // highest lane of the group
+    const uint32_t below = __popc(peers & lt);
+    if (j < hi) {
+      const uint32_t dst = wh[d] + below;
+      kout[dst] = k;
+      pout[dst] = pin[j];
+    }
+    __syncwarp();
+    if (j < hi && lane == leader) wh[d] += below + 1;
+    __syncwarp();
+  }
+  __syncthreads();
+}
+
+struct LocalOut {
+  double* pts;
+  double* q;
+  int64_t* perm;
+  uint64_t* boxes;
+  uint64_t* ne;
+  int64_t* bm;
+  unsigned long long* bmp[2];  // level-L occupancy bitmaps (may be null)
+  int64_t* kinfo;
+};
+
+// Ranking inside a bucket: with HEADS and <= 2^kLcSmallBits boxes per bucket,
+// per-box counts (shared atomics), unstable placement into box segments and a
+// rank of each point among its box's points by combined input index (boxes
+// hold a handful of points; a box of more than 64 falls back).  Otherwise a
+// stable LSD sort of the composite (low key bits, range id): a range's chunks
+// land in its input order, so range id then arrival order is input order.
+//
+// HEADS: box heads go to the occupancy bitmap plus a bucket-local list of
+// head positions (hpos[bs + h]); k_bkt_heads later writes bookmarks and
+// non-empty keys at their global box ranks, taken from the bitmap's rank
+// directory (no cross-bucket dependency here).  Without HEADS (sort_points:
+// no bitmaps) the box ranks come from a decoupled look-back over buckets.
+template <typename CK, bool NARROW, bool HEADS>
+__global__ void __launch_bounds__(kLcThreads)
+    k_bkt_local(const double* __restrict__ rec, uint32_t* __restrict__ idx,
+                const uint32_t* __restrict__ bstart, const BucketGeo g, int level,
+                const LocalOut o, uint64_t* __restrict__ states, uint32_t* __restrict__ ticket,
+                const uint32_t* __restrict__ maxb, uint32_t* __restrict__ fail) {
+  extern __shared__ __align__(128) unsigned char lc_smem[];
+  double* s_rec = reinterpret_cast<double*>(lc_smem);                   // [cap][4]
+  uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_rec + 4 * kLcCap);    // [cap]
+  CK* k0 = reinterpret_cast<CK*>(s_idx + kLcCap);
+  CK* k1 = k0 + kLcCap;
+  uint16_t* p0 = reinterpret_cast<uint16_t*>(k1 + kLcCap);
+  uint16_t* p1 = p0 + kLcCap;
+  uint32_t* s_wh = reinterpret_cast<uint32_t*>(p1 + kLcCap);
+  uint64_t* s_misc = reinterpret_cast<uint64_t*>(s_wh + kLcWarps * kLcBins);  // 16 B aligned
+  uint32_t* s_red = reinterpret_cast<uint32_t*>(s_misc + 4);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (__ldg(maxb) > (uint32_t)kLcCap) {  // some bucket overflows: general path
+    if (blockIdx.x == 0 && tid == 0) atomicOr(fail, 1u);
+    return;
+  }
+  uint64_t* bar = s_misc + 2;
+  if (tid == 0) {
+    s_misc[0] = HEADS ? (uint64_t)blockIdx.x : (uint64_t)atomicAdd(ticket, 1u);
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int64_t tile = (int64_t)s_misc[0];
+  const int b = (int)tile;
+  const int64_t bs = bstart[b];
+  const int B = (int)(bstart[b + 1] - bs);
+  const int set = b >> g.bb;
+  const uint64_t prefix = (uint64_t)(b & ((1 << g.bb) - 1)) << g.shift;
+  const uint64_t lmask = (1ull << g.shift) - 1ull;
+  const int64_t n = g.n, m = g.m, tot = n + m;
+
+  // phase 0: bulk copy of the bucket's records (TMA), source indices by LDG
+  if (tid == 0 && B > 0) {
+    const uint32_t bytes = (uint32_t)B * 32u;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
+            "r"(smem_u32(s_rec)),
+        "l"(rec + 4 * (size_t)bs), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+  }
+  if (set == 0)
+    for (int j = tid; j < B; j += kLcThreads) s_idx[j] = __ldg(idx + bs + j);
+  if (B > 0) {
+    uint32_t done = 0;
+    while (!done)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
+          "selp.u32 %0, 1, 0, p;\n\t}"
+          : "=r"(done)
+          : "r"(smem_u32(bar))
+          : "memory");
+  }
+  __syncthreads();
+  // phase 1: low key bits and combined input index of every record; with
+  // HEADS and <= 2^12 boxes per bucket also the per-box counts
+  const double grid = (double)(1ll << level);
+  const bool small = HEADS && g.shift <= kLcSmallBits;
+  const int nbins = 1 << (g.shift <= kLcSmallBits ? g.shift : 0);
+  if (small)
+    for (int i = tid; i < nbins; i += kLcThreads) s_wh[i] = 0;
+  __syncthreads();
+  for (int j = tid; j < B; j += kLcThreads) {
+    const double* r = s_rec + 4 * j;
+    const uint64_t key = encode_any<NARROW>(r[0], r[1], r[2], level, grid);
+    const uint32_t ci = set == 0 ? s_idx[j] : (uint32_t)(n + __double_as_longlong(r[3]));
+    const uint32_t lk = (uint32_t)(key & lmask);
+    if (small) {
+      k0[j] = (CK)lk;
+      s_idx[j] = ci;
+      atomicAdd(&s_wh[lk], 1u);
+    } else {
+      k0[j] = ((CK)(key & lmask) << g.wbits) | (CK)(ci >> g.rbits);
+    }
+    p0[j] = (uint16_t)j;
+  }
+  __syncthreads();
+  bool ranked = false;
+  if (small) {
+    // per-box counts -> (count << 16 | start) cursors; heads straight from the
+    // non-empty boxes; the largest box picks the ranking method
+    constexpr int kBpt = (1 << kLcSmallBits) / kLcThreads;
+    uint32_t c[kBpt];
+    uint32_t csum = 0, nz = 0, cmax = 0;
+#pragma unroll
+    for (int e = 0; e < kBpt; ++e) {
+      const int i = tid * kBpt + e;
+      c[e] = i < nbins ? s_wh[i] : 0u;
+      csum += c[e];
+      nz += c[e] ? 1u : 0u;
+      cmax = c[e] > cmax ? c[e] : cmax;
+    }
+    const uint32_t packed = (nz << 16) | csum;  // both < 2^16 per thread
+    uint32_t wt;
+    uint32_t x = warp_excl_scan(packed, wt);
+    cmax = __reduce_max_sync(0xffffffffu, cmax);
+    if (lane == 0) {
+      s_red[warp] = wt;
+      s_red[8 + warp] = cmax;
+    }
+    __syncthreads();
+    uint32_t mx = 0;
+    for (int i = 0; i < kLcWarps; ++i) {
+      x += i < warp ? s_red[i] : 0u;
+      mx = s_red[8 + i] > mx ? s_red[8 + i] : mx;
+    }
+    ranked = mx <= 64;
+    uint32_t start = x & 0xFFFFu, hidx = x >> 16;
+    unsigned long long* bm = set ? o.bmp[1] : o.bmp[0];
+    uint32_t* hp = idx + bs;
+#pragma unroll
+    for (int e = 0; e < kBpt; ++e) {
+      const int i = tid * kBpt + e;
+      if (i < nbins) {
+        s_wh[i] = (c[e] << 16) | start;
+        if (c[e]) {
+          const uint64_t mk = prefix | (uint64_t)i;
+          if (bm) atomicOr(bm + (mk >> 6), 1ull << (mk & 63));
+          hp[hidx] = (uint32_t)(bs + start - (set ? n : 0));
+          ++hidx;
+        }
+      }
+      start += c[e];
+    }
+    __syncthreads();
+    if (!ranked) {  // a crowded box: fall back to the LSD passes below
+      for (int j = tid; j < B; j += kLcThreads)
+        k0[j] = ((CK)k0[j] << g.wbits) | (CK)(s_idx[j] >> g.rbits);
+      __syncthreads();
+    }
+  }
+  if (ranked) {
+    // unstable placement into box segments, then rank inside the box by the
+    // combined input index (unique): position = start + #smaller indices
+    CK* tci = k1;
+    uint16_t* tj = p1;
+    for (int j = tid; j < B; j += kLcThreads) {
+      const uint32_t slot = atomicAdd(&s_wh[(uint32_t)k0[j]], 1u) & 0xFFFFu;
+      tci[slot] = (CK)s_idx[j];
+      tj[slot] = (uint16_t)j;
+    }
+    __syncthreads();
+    for (int t = tid; t < B; t += kLcThreads) {
+      const uint32_t ci = (uint32_t)tci[t];
+      const int j = tj[t];
+      const uint32_t v = s_wh[(uint32_t)k0[j]];
+      const uint32_t end = v & 0xFFFFu, cnt = v >> 16;
+      uint32_t rank = 0;
+#pragma unroll 4
+      for (uint32_t u = end - cnt; u < end; ++u) rank += (uint32_t)tci[u] < ci ? 1u : 0u;
+      p0[end - cnt + rank] = (uint16_t)j;
+    }
+    __syncthreads();
+    // phase 4 (ranked): outputs in sorted order; heads were written above
+    for (int pos = tid; pos < B; pos += kLcThreads) {
+      const int64_t p = bs + pos;
+      const int j = p0[pos];
+      const double* r = s_rec + 4 * j;
+      double* po = o.pts + 3 * p;
+      po[0] = r[0];
+      po[1] = r[1];
+      po[2] = r[2];
+      if (set == 0) {
+        if (o.q) o.q[p] = r[3];
+        o.perm[p] = (int64_t)s_idx[j];
+      } else {
+        o.perm[p] = __double_as_longlong(r[3]);
+      }
+      o.boxes[p] = prefix | (uint64_t)k0[j];
+    }
+    return;
+  }
+  // phase 2: stable LSD passes (range id first, then the key bits)
+  CK* kc = k0;
+  uint16_t* pc = p0;
+  const int cbits = g.shift + g.wbits;
+  for (int ds = 0; ds < cbits; ds += kLcDigit) {
+    const int db = cbits - ds < kLcDigit ? cbits - ds : kLcDigit;
+    CK* ko = kc == k0 ? k1 : k0;
+    uint16_t* po = pc == p0 ? p1 : p0;
+    lc_pass<CK>(kc, pc, ko, po, B, ds, db, s_wh, s_red);
+    kc = ko;
+    pc = po;
+  }
+  const int wb = g.wbits;
+  int64_t hbase = 0;
+  if (!HEADS) {
+    // phase 3: head count, box-rank base by look-back over buckets
+    uint32_t hc = 0;
+    for (int j = tid; j < B; j += kLcThreads)
+      hc += (j == 0 || (kc[j] >> wb) != (kc[j - 1] >> wb)) ? 1u : 0u;
+    hc = __reduce_add_sync(0xffffffffu, hc);
+    if (lane == 0) s_red[warp] = hc;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t heads = 0;
+      for (int i = 0; i < kLcWarps; ++i) heads += s_red[i];
+      uint64_t* st = states + tile;
+      uint64_t excl = 0;
+      if (tile == 0) {
+        st_state(st, kStInclusive | heads);
+      } else {
+        st_state(st, kStAggregate | heads);
+        excl = lookback(states, tile, 0, 1);
+        st_state(st, kStInclusive | (excl + heads));
+      }
+      s_misc[1] = excl;
+    }
+    __syncthreads();
+    hbase = (int64_t)s_misc[1];
+  }
+  unsigned long long* bmp = set ? o.bmp[1] : o.bmp[0];
+  uint32_t* hpos = idx + bs;  // HEADS: this bucket's idx slots are free again
+  const unsigned lt = lanemask_lt();
+  // phase 4: outputs in sorted order (chunks of kLcThreads, scan of heads)
+  for (int j0 = 0; j0 < B; j0 += kLcThreads) {
+    const int j = j0 + tid;
+    const bool ok = j < B;
+    bool head = false;
+    uint64_t lk = 0;
+    if (ok) {
+      lk = (uint64_t)(kc[j] >> wb);
+      head = j == 0 || (uint64_t)(kc[j - 1] >> wb) != lk;
+    }
+    const unsigned hb = __ballot_sync(0xffffffffu, head);
+    if (lane == 0) s_red[8 + warp] = __popc(hb);
+    __syncthreads();
+    uint32_t woff = 0, ctot = 0;
+#pragma unroll
+    for (int i = 0; i < kLcWarps; ++i) {
+      const uint32_t c = s_red[8 + i];
+      woff += i < warp ? c : 0u;
+      ctot += c;
+    }
+    if (ok) {
+      const int64_t p = bs + j;  // combined sorted position
+      const int pl = pc[j];
+      const double* r = s_rec + 4 * pl;
+      const uint64_t mk = prefix | lk;
+      double* po = o.pts + 3 * p;
+      po[0] = r[0];
+      po[1] = r[1];
+      po[2] = r[2];
+      if (set == 0) {
+        if (o.q) o.q[p] = r[3];
+        o.perm[p] = (int64_t)s_idx[pl];
+      } else {
+        o.perm[p] = __double_as_longlong(r[3]);
+      }
+      o.boxes[p] = mk;
+      const int64_t incl = hbase + woff + __popc(hb & (lt | (1u << lane)));
+      if (head) {
+        if (bmp) atomicOr(bmp + (mk >> 6), 1ull << (mk & 63));
+        if (HEADS) {
+          hpos[incl - 1] = (uint32_t)(p - (set ? n : 0));
+        } else {
+          const int64_t jg = incl - 1;
+          o.ne[jg] = mk;
+          o.bm[jg + set] = p - (set ? n : 0);
+        }
+      }
+      if (!HEADS) {
+        if (p == n - 1) {
+          o.kinfo[0] = incl;
+          o.bm[incl] = n;
+          if (m == 0) o.bm[incl + 1] = 0;
+        }
+        if (p == tot - 1 && m > 0) {
+          o.kinfo[1] = incl;
+          o.bm[incl + 1] = m;
+          if (n == 0) {
+            o.bm[0] = 0;
+            o.kinfo[0] = 0;
+          }
+        }
+      }
+    }
+    hbase += ctot;
+    __syncthreads();  // s_red[8..] reused by the next chunk
+  }
+}
+
+// Bookmarks and non-empty keys at their global box ranks (HEADS variant):
+// one warp per bucket walks the bucket's words of the level-L bitmap; the
+// h-th set bit is the bucket's h-th box, its rank = rank directory + prefix
+// popcount, its first point = hpos[bs + h].
+struct HeadsParams {
+  const uint64_t* bmp[2];  // level-L bitmaps (src, recv)
+  const uint32_t* dir[2];  // their rank directories
+  const int64_t* ktot_src;  // K_s (device, from k_rank)
+  const int64_t* ktot_recv; // K_r
+  const uint32_t* bstart;
+  const uint32_t* hpos;
+  uint64_t* ne;
+  int64_t* bm;
+  int64_t* kinfo;
+};
+
+__global__ void __launch_bounds__(256)
+    k_bkt_heads(const __grid_constant__ HeadsParams hp, const BucketGeo g) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int b = blockIdx.x * 8 + warp;
+  const int64_t ks = *hp.ktot_src;
+  if (b == 0 && lane == 0) {
+    const int64_t kr = *hp.ktot_recv;
+    hp.bm[ks] = g.n;
+    hp.bm[ks + 1 + kr] = g.m;
+    hp.kinfo[0] = ks;
+    hp.kinfo[1] = ks + kr;
+  }
+  if (b >= g.nb) return;
+  const int set = b >> g.bb;
+  const uint64_t key0 = (uint64_t)(b & ((1 << g.bb) - 1)) << g.shift;
+  const uint64_t nbits = 1ull << g.shift;
+  const uint64_t* bmp = set ? hp.bmp[1] : hp.bmp[0];
+  const uint32_t* dir = set ? hp.dir[1] : hp.dir[0];
+  const uint32_t* hpos = hp.hpos + hp.bstart[b];
+  uint64_t* ne = hp.ne + (set ? ks : 0);
+  int64_t* bm = hp.bm + (set ? ks + 1 : 0);
+  const int64_t w0 = (int64_t)(key0 >> 6);
+  const uint64_t below0 = (key0 & 63) ? (__ldg(bmp + w0) & ((1ull << (key0 & 63)) - 1ull)) : 0ull;
+  const int64_t rank0 = (int64_t)__ldg(dir + w0) + __popcll(below0);
+  const unsigned lt = lanemask_lt();
+  int64_t h = 0;
+  // lane = box: 32 consecutive keys per step; all-zero 64-bit words skipped
+  for (uint64_t off = 0; off < nbits; off += 32) {
+    const uint64_t key = key0 + off + lane;
+    const uint64_t word = __ldg(bmp + (key >> 6));
+    if (__all_sync(0xffffffffu, word == 0)) {  // skip the rest of an empty word
+      off = ((key0 + off + 64) & ~63ull) - key0 - 32;
+      continue;
+    }
+    const bool occ = off + lane < nbits && ((word >> (key & 63)) & 1ull);
+    const unsigned ballot = __ballot_sync(0xffffffffu, occ);
+    if (occ) {
+      const int64_t at = h + __popc(ballot & lt);
+      ne[rank0 + at] = key;
+      bm[rank0 + at] = (int64_t)__ldg(hpos + at);
+    }
+    h += __popc(ballot);
+  }
+}
+
+}  // namespace fmmb

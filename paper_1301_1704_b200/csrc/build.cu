@@ -20,6 +20,7 @@
 
 #include "internal.h"
 #include "common.cuh"
+#include "bucket.cuh"
 #include "finalize.cuh"
 #include "lists.cuh"
 #include "sort.cuh"
@@ -76,6 +77,26 @@ extern "C" fmmb_status fmmb_create(int device, fmmb_handle_t* out) {
                        (int)onesweep_smem_bytes(8));
   cudaFuncSetAttribute(k_onesweep<uint64_t, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)onesweep_smem_bytes(8));
+  cudaFuncSetAttribute(k_bkt_hist<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (2 << kBucketBitsMax) * (int)sizeof(uint32_t));
+  cudaFuncSetAttribute(k_bkt_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (2 << kBucketBitsMax) * (int)sizeof(uint32_t));
+  cudaFuncSetAttribute(k_bkt_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)scatter_smem_bytes(kSMaxWarps));
+  cudaFuncSetAttribute(k_bkt_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)scatter_smem_bytes(kSMaxWarps));
+#define FMMB_LCATTR(CK, NW, HD)                                                        \
+  cudaFuncSetAttribute(k_bkt_local<CK, NW, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                       (int)lc_smem_bytes<CK>())
+  FMMB_LCATTR(uint32_t, true, true);
+  FMMB_LCATTR(uint32_t, true, false);
+  FMMB_LCATTR(uint32_t, false, true);
+  FMMB_LCATTR(uint32_t, false, false);
+  FMMB_LCATTR(uint64_t, true, true);
+  FMMB_LCATTR(uint64_t, true, false);
+  FMMB_LCATTR(uint64_t, false, true);
+  FMMB_LCATTR(uint64_t, false, false);
+#undef FMMB_LCATTR
   cudaFuncSetAttribute(k_gather<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)gather_smem_bytes());
   cudaFuncSetAttribute(k_gather<uint64_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -102,6 +123,14 @@ extern "C" const char* fmmb_last_error(fmmb_handle_t h) {
 }
 
 extern "C" int64_t fmmb_last_launch_count(fmmb_handle_t h) { return h ? h->launches : -1; }
+
+extern "C" fmmb_status fmmb_set_sort_path(fmmb_handle_t h, int path) {
+  if (!h || path < 0 || path > 2) return FMMB_ERR_ARG;
+  h->sort_path = path;
+  return FMMB_OK;
+}
+
+extern "C" int fmmb_last_sort_path(fmmb_handle_t h) { return h ? h->last_sort_path : -1; }
 
 int lists_lmin_host(int L) { return L >= 2 ? 2 : L; }
 
@@ -145,7 +174,141 @@ struct BuildPlanHost {  // mirrored in the pinned readback block
   int64_t seg_totals[kMaxLevel + 1];
   int64_t kinfo[2];
   uint32_t err;
+  uint32_t fail;  // bucket path overflowed its shared-memory capacity
 };
+
+// ---- sort phase, fast path: payload-carrying bucket sort (bucket.cuh)
+struct BucketRun {  // scratch that outlives the sort phase (heads pass)
+  char* scratch = nullptr;
+  BucketGeo g{};
+  const uint32_t* bstart = nullptr;
+  const uint32_t* hpos = nullptr;
+};
+
+template <typename CK, bool NARROW, bool HEADS>
+void launch_local(const double* rec, uint32_t* idx, const uint32_t* bstart, const BucketGeo& g,
+                  int L, const LocalOut& o, uint64_t* lst, uint32_t* ctl, uint32_t* fail,
+                  cudaStream_t s) {
+  k_bkt_local<CK, NARROW, HEADS><<<(unsigned)g.nb, kLcThreads, lc_smem_bytes<CK>(), s>>>(
+      rec, idx, bstart, g, L, o, lst, ctl + 1, ctl + 2, fail);
+}
+
+template <bool NARROW>
+void launch_hs(const double* src, const double* q, const double* recv, const BucketGeo& g,
+               int L, uint32_t* mat, uint32_t* bstart, uint32_t* cursor, uint64_t* sst,
+               uint32_t* ctl, double* rec, uint32_t* idx, uint32_t* err, cudaStream_t s) {
+  k_bkt_hist<NARROW><<<(unsigned)g.hgrid, kHThreads, (size_t)g.nb * 4, s>>>(src, recv, g, L,
+                                                                             mat, err);
+  k_bkt_scan<<<(unsigned)ceil_div(g.nb, kScanBuckets), 256, 0, s>>>(mat, g, bstart, cursor, sst,
+                                                                    ctl + 0, ctl + 2);
+  k_bkt_scatter<NARROW><<<(unsigned)ceil_div(g.nranges, g.swarps), (unsigned)g.swarps * 32,
+                          scatter_smem_bytes(g.swarps), s>>>(src, q, recv, g, L, cursor, rec, idx);
+}
+
+fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int64_t n,
+                        const double* recv, int64_t m, int L, const LocalOut& o, bool heads,
+                        BuildPlanHost* dplan, cudaStream_t s, int64_t& launches,
+                        BucketRun& run) {
+  const BucketGeo g = bucket_geo(L, n, m, h->num_sms);
+  const int64_t tot = n + m;
+  Carver c;
+  const size_t o_sst = c.take<uint64_t>(ceil_div(g.nb, kScanBuckets));
+  const size_t o_lst = c.take<uint64_t>(g.nb);
+  const size_t o_ctl = c.take<uint32_t>(4);  // [0] scan ticket, [1] local ticket, [2] max bucket
+  const size_t zero_bytes = c.off;
+  const size_t o_mat = c.take<uint32_t>((int64_t)g.hgrid * g.nb);
+  const size_t o_bs = c.take<uint32_t>(g.nb + 1);
+  const size_t o_cur = c.take<uint32_t>((int64_t)g.nb * kCursorStride);
+  const size_t o_rec = c.take<double>(4 * tot);
+  const size_t o_idx = c.take<uint32_t>(tot);
+  char* w = nullptr;
+  if (cudaMallocAsync((void**)&w, c.off, s) != cudaSuccess)
+    return fmmb_fail(h, FMMB_ERR_CUDA, "bucket-sort scratch of %zu bytes failed", c.off);
+  cudaMemsetAsync(w, 0, zero_bytes, s);
+  uint32_t* ctl = (uint32_t*)(w + o_ctl);
+  uint32_t* mat = (uint32_t*)(w + o_mat);
+  uint32_t* bstart = (uint32_t*)(w + o_bs);
+  uint32_t* cursor = (uint32_t*)(w + o_cur);
+  double* rec = (double*)(w + o_rec);
+  uint32_t* idx = (uint32_t*)(w + o_idx);
+  uint64_t* sst = (uint64_t*)(w + o_sst);
+  uint64_t* lst = (uint64_t*)(w + o_lst);
+  const bool narrow = L <= 10;
+  if (narrow)
+    launch_hs<true>(src, q, recv, g, L, mat, bstart, cursor, sst, ctl, rec, idx, &dplan->err, s);
+  else
+    launch_hs<false>(src, q, recv, g, L, mat, bstart, cursor, sst, ctl, rec, idx, &dplan->err, s);
+  const bool ck32 = g.shift + g.wbits <= 32;
+#define FMMB_LOCAL(CK, NW, HD) \
+  launch_local<CK, NW, HD>(rec, idx, bstart, g, L, o, lst, ctl, &dplan->fail, s)
+  if (heads) {
+    if (narrow) { if (ck32) FMMB_LOCAL(uint32_t, true, true); else FMMB_LOCAL(uint64_t, true, true); }
+    else { if (ck32) FMMB_LOCAL(uint32_t, false, true); else FMMB_LOCAL(uint64_t, false, true); }
+  } else {
+    if (narrow) { if (ck32) FMMB_LOCAL(uint32_t, true, false); else FMMB_LOCAL(uint64_t, true, false); }
+    else { if (ck32) FMMB_LOCAL(uint32_t, false, false); else FMMB_LOCAL(uint64_t, false, false); }
+  }
+#undef FMMB_LOCAL
+  launches += 4;
+  run.scratch = w;
+  run.g = g;
+  run.bstart = bstart;
+  run.hpos = idx;
+  return FMMB_OK;
+}
+
+// ---- sort phase, general path: encode + Onesweep LSD + permuted gather
+template <typename KeyT>
+fmmb_status sort_onesweep(fmmb_handle_t h, const double* src, const double* q, int64_t n,
+                          const double* recv, int64_t m, int L, const LocalOut& o,
+                          BuildPlanHost* dplan, cudaStream_t s, int64_t& launches) {
+  const int64_t tot = n + m;
+  const int npass = sort_passes(L);
+  const int64_t sort_tiles = ceil_div(tot, kSortTile);
+  const int64_t gather_tiles = ceil_div(tot, kGTile);
+  Carver c;
+  const size_t o_hist = c.take<uint32_t>(npass * kBins);
+  const size_t o_tc = c.take<uint32_t>(16);
+  const size_t o_sst = c.take<uint64_t>((int64_t)npass * sort_tiles * kBins);
+  const size_t o_gst = c.take<uint64_t>(gather_tiles);
+  const size_t zero_bytes = c.off;
+  const size_t o_ka = c.take<KeyT>(tot), o_kb = c.take<KeyT>(tot);
+  const size_t o_va = c.take<uint32_t>(tot), o_vb = c.take<uint32_t>(tot);
+  char* w = nullptr;
+  if (cudaMallocAsync((void**)&w, c.off, s) != cudaSuccess)
+    return fmmb_fail(h, FMMB_ERR_CUDA, "sort scratch of %zu bytes failed", c.off);
+  cudaMemsetAsync(w, 0, zero_bytes, s);
+  uint32_t* hist = (uint32_t*)(w + o_hist);
+  uint32_t* tc = (uint32_t*)(w + o_tc);
+  KeyT* ka = (KeyT*)(w + o_ka);
+  KeyT* kb = (KeyT*)(w + o_kb);
+  uint32_t* va = (uint32_t*)(w + o_va);
+  uint32_t* vb = (uint32_t*)(w + o_vb);
+  const int eg = (int)std::min<int64_t>(ceil_div(tot, kSortThreads), (int64_t)h->num_sms * 8);
+  k_encode_hist<KeyT><<<eg, kSortThreads, 0, s>>>(src, n, recv, m, L, npass, ka, hist,
+                                                  &dplan->err);
+  ++launches;
+  uint64_t* sst = (uint64_t*)(w + o_sst);
+  const size_t smem = onesweep_smem_bytes(sizeof(KeyT));
+  for (int ps = 0; ps < npass; ++ps) {
+    uint64_t* st = sst + (size_t)ps * sort_tiles * kBins;
+    if (ps == 0)
+      k_onesweep<KeyT, true><<<(unsigned)sort_tiles, kSortThreads, smem, s>>>(
+          ka, nullptr, kb, vb, tot, 0, hist, st, tc + ps);
+    else
+      k_onesweep<KeyT, false><<<(unsigned)sort_tiles, kSortThreads, smem, s>>>(
+          ka, va, kb, vb, tot, kRadixBits * ps, hist + ps * kBins, st, tc + ps);
+    ++launches;
+    std::swap(ka, kb);
+    std::swap(va, vb);
+  }
+  k_gather<KeyT><<<(unsigned)gather_tiles, kGThreads, gather_smem_bytes(), s>>>(
+      ka, va, n, m, L, src, q, recv, o.pts, o.q, o.perm, o.boxes, o.ne, o.bm, o.bmp[0], o.bmp[1],
+      (uint64_t*)(w + o_gst), tc + 8, o.kinfo);
+  ++launches;
+  cudaFreeAsync(w, s);
+  return FMMB_OK;
+}
 
 template <typename KeyT>
 fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int64_t n,
@@ -153,9 +316,6 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
                        void* ctx, fmmb_structures* out, cudaEvent_t* ev,
                        cudaStream_t s, bool lists) {
   const int64_t tot = n + m;
-  const int npass = sort_passes(L);
-  const int64_t sort_tiles = ceil_div(tot, kSortTile);
-  const int64_t gather_tiles = ceil_div(tot, kGTile);
   const int stride = L + 1;
 
   // bitmap segment layout: seg = set*(L+1)+l, each starting on a rank tile
@@ -187,18 +347,13 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
 
   // ---- workspace: [zeroed control | rest]
   Carver z;
-  const size_t o_hist = z.take<uint32_t>(npass * kBins);
   const size_t o_tc = z.take<uint32_t>(16);  // tile counters
-  const size_t o_sst = z.take<uint64_t>((int64_t)npass * sort_tiles * kBins);
-  const size_t o_gst = z.take<uint64_t>(gather_tiles);
   const size_t o_rst = z.take<uint64_t>(rank_tiles);
   const size_t o_lst = z.take<uint64_t>(scan_tiles_cap);
   const size_t o_plan = z.take<BuildPlanHost>(1);
   const size_t o_bmp = z.take<uint64_t>(bmp_words);
   const size_t zero_bytes = z.off;
   const size_t o_dir = z.take<uint32_t>(bmp_words);
-  const size_t o_ka = z.take<KeyT>(tot), o_kb = z.take<KeyT>(tot);
-  const size_t o_va = z.take<uint32_t>(tot), o_vb = z.take<uint32_t>(tot);
   const size_t o_lowkeys = z.take<uint64_t>(2 * (1 + 8));  // levels 0,1 keys
   const size_t o_cnt = z.take<uint32_t>(cnt_cap);
   const size_t o_lay = z.take<ListsLayout>(1);
@@ -207,7 +362,6 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
   if (cudaMallocAsync((void**)&ws, z.off, s) != cudaSuccess)
     return fmmb_fail(h, FMMB_ERR_CUDA, "workspace allocation of %zu bytes failed", z.off);
   auto W = [&](size_t o) { return (void*)(ws + o); };
-  uint32_t* hist = (uint32_t*)W(o_hist);
   uint32_t* tc = (uint32_t*)W(o_tc);
   BuildPlanHost* dplan = (BuildPlanHost*)W(o_plan);
   uint64_t* bmp = (uint64_t*)W(o_bmp);
@@ -241,131 +395,146 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
   int64_t* bm_out = (int64_t*)A(a_bm);
   uint64_t* ne_out = (uint64_t*)A(a_ne);
 
+  LocalOut lo{};
+  lo.pts = pts_out;
+  lo.q = q ? (double*)A(a_q) : nullptr;
+  lo.perm = (int64_t*)A(a_perm);
+  lo.boxes = (uint64_t*)A(a_boxes);
+  lo.ne = ne_out;
+  lo.bm = bm_out;
+  lo.bmp[0] = lists ? (unsigned long long*)(bmp + rp.word_off[L]) : nullptr;
+  lo.bmp[1] = lists ? (unsigned long long*)(bmp + rp.word_off[stride + L]) : nullptr;
+  lo.kinfo = dplan->kinfo;
+
   int64_t launches = 0;
-#define FMMB_LAUNCHED() \
-  do {                  \
-    ++launches;         \
-  } while (0)
-
-  if (ev) cudaEventRecord(ev[0], s);
-  cudaMemsetAsync(ws, 0, zero_bytes, s);
-  if (tot == 0) cudaMemsetAsync(bm_out, 0, 2 * sizeof(int64_t), s);
-
-  // ---- K1/K2: encode + radix sort
-  KeyT* ka = (KeyT*)W(o_ka);
-  KeyT* kb = (KeyT*)W(o_kb);
-  uint32_t* va = (uint32_t*)W(o_va);
-  uint32_t* vb = (uint32_t*)W(o_vb);
-  if (tot > 0) {
-    const int eg = (int)std::min<int64_t>(ceil_div(tot, kSortThreads), (int64_t)h->num_sms * 8);
-    k_encode_hist<KeyT><<<eg, kSortThreads, 0, s>>>(src, n, recv, m, L, npass, ka, hist,
-                                                    &dplan->err);
-    FMMB_LAUNCHED();
-    uint64_t* sst = (uint64_t*)W(o_sst);
-    const size_t smem = onesweep_smem_bytes(sizeof(KeyT));
-    for (int ps = 0; ps < npass; ++ps) {
-      uint64_t* st = sst + (size_t)ps * sort_tiles * kBins;
-      if (ps == 0)
-        k_onesweep<KeyT, true><<<(unsigned)sort_tiles, kSortThreads, smem, s>>>(
-            ka, nullptr, kb, vb, tot, 0, hist, st, tc + ps);
-      else
-        k_onesweep<KeyT, false><<<(unsigned)sort_tiles, kSortThreads, smem, s>>>(
-            ka, va, kb, vb, tot, kRadixBits * ps, hist + ps * kBins, st, tc + ps);
-      FMMB_LAUNCHED();
-      std::swap(ka, kb);
-      std::swap(va, vb);
-    }
-    // ---- K3/K4: gather + bookmarks + level-L bitmaps
-    k_gather<KeyT><<<(unsigned)gather_tiles, kGThreads, gather_smem_bytes(), s>>>(
-        ka, va, n, m, L, src, q, recv, pts_out, q ? (double*)A(a_q) : nullptr,
-        (int64_t*)A(a_perm), (uint64_t*)A(a_boxes), ne_out, bm_out,
-        lists ? (unsigned long long*)(bmp + rp.word_off[L]) : nullptr,
-        lists ? (unsigned long long*)(bmp + rp.word_off[stride + L]) : nullptr,
-        (uint64_t*)W(o_gst), tc + 8, dplan->kinfo);
-    FMMB_LAUNCHED();
-  }
-  if (ev) cudaEventRecord(ev[1], s);
-
-  // ---- K5: bitmap pyramid (big levels one launch each, the rest in one CTA)
-  int l = lists ? L : 0;
-  while (l >= 1 && level_words(l - 1) > 4096) {
-    const int64_t nc = level_words(l - 1);
-    k_pyramid<<<(unsigned)ceil_div(2 * nc, 256), 256, 0, s>>>(
-        bmp + rp.word_off[l], bmp + rp.word_off[l - 1], bmp + rp.word_off[stride + l],
-        bmp + rp.word_off[stride + l - 1], nc);
-    FMMB_LAUNCHED();
-    --l;
-  }
-  if (l >= 1) {
-    PyramidTail pt{};
-    for (int k = 0; k <= L; ++k) {
-      pt.lvl[0][k] = bmp + rp.word_off[k];
-      pt.lvl[1][k] = bmp + rp.word_off[stride + k];
-      pt.nwords[k] = level_words(k);
-    }
-    pt.from_level = l;
-    k_pyramid_tail<<<1, 1024, 0, s>>>(pt);
-    FMMB_LAUNCHED();
-  }
-  // ---- rank directory, totals and per-level directory keys
-  rp.bmp = bmp;
-  rp.dir = dir;
-  rp.states = (uint64_t*)W(o_rst);
-  rp.tile_counter = tc + 9;
-  rp.totals = dplan->ktot;
-  uint64_t* lowkeys = (uint64_t*)W(o_lowkeys);
-  for (int set = 0; set < 2; ++set)
-    for (int k = 0; k <= L; ++k) {
-      uint64_t* dst = nullptr;
-      if (k < L) {
-        if (k == 0) dst = lowkeys + set * 9;
-        else if (k == 1) dst = lowkeys + set * 9 + 1;
-        else if (lists) dst = (uint64_t*)A(a_dir[set][k]);
-      }
-      rp.keys_out[set * stride + k] = dst;
-    }
-  if (lists) {
-    k_rank<<<(unsigned)rank_tiles, kRThreads, 0, s>>>(rp);
-    FMMB_LAUNCHED();
-  }
-  if (ev) cudaEventRecord(ev[2], s);
-
+  bool fast = h->sort_path != 2 && tot > 0;
+  BuildPlanHost* hp = (BuildPlanHost*)h->pinned;
   ListsParams lp{};
   int64_t nwork_cap = 0;
-  if (lists) {
-    lp.level = L;
-    lp.ktot = dplan->ktot;
-    lp.bmp = bmp;
-    lp.dir = dir;
-    for (int set = 0; set < 2; ++set)
-      for (int k = 0; k <= L; ++k) lp.bmp_off[set][k] = rp.word_off[set * stride + k];
-    for (int k = 0; k < L; ++k) lp.rkeys[k] = rp.keys_out[stride + k];
-    lp.counts = (uint32_t*)W(o_cnt);
-    lp.bm[0] = (int64_t*)A(a_lbm[0]);
-    for (int k = 2; k <= L; ++k) lp.bm[k] = (int64_t*)A(a_lbm[k]);
-    for (int k = std::max(1, lists_lmin_host(L)); k <= L; ++k) nwork_cap += cap_level(m, k - 1);
-    if (L == 0) nwork_cap = 1;
-    const int lgrid = (int)std::max<int64_t>(
-        1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * 16));
-    ListsLayout* glay = (ListsLayout*)W(o_lay);
-    k_lists_plan<<<1, 32, 0, s>>>(lp, glay);
-    FMMB_LAUNCHED();
-    k_lists_count<<<lgrid, kLThreads, 0, s>>>(lp, glay);
-    FMMB_LAUNCHED();
-    k_lists_scan<<<(unsigned)std::max<int64_t>(1, scan_tiles_cap), kScanThreads, 0, s>>>(
-        lp, glay, (uint64_t*)W(o_lst), tc + 10, dplan->seg_totals);
-    FMMB_LAUNCHED();
-  }
-  if (ev) cudaEventRecord(ev[3], s);
+  for (int attempt = 0;; ++attempt) {
+    if (ev) cudaEventRecord(ev[0], s);
+    cudaMemsetAsync(ws, 0, zero_bytes, s);
+    if (tot == 0) cudaMemsetAsync(bm_out, 0, 2 * sizeof(int64_t), s);
 
-  // ---- sizes back to the host (the build's single synchronisation)
-  BuildPlanHost* hp = (BuildPlanHost*)h->pinned;
-  cudaMemcpyAsync(hp, dplan, sizeof(BuildPlanHost), cudaMemcpyDeviceToHost, s);
-  cudaError_t ce = cudaStreamSynchronize(s);
-  if (ce != cudaSuccess) {
-    cudaFreeAsync(ws, s);
-    return fmmb_fail(h, FMMB_ERR_CUDA, "build phase A failed: %s", cudaGetErrorString(ce));
+    // ---- K1-K4: sort both sets into the reference layout
+    BucketRun brun;
+    if (tot > 0) {
+      const fmmb_status st =
+          fast ? sort_bucket(h, src, q, n, recv, m, L, lo, lists, dplan, s, launches, brun)
+               : sort_onesweep<KeyT>(h, src, q, n, recv, m, L, lo, dplan, s, launches);
+      if (st != FMMB_OK) {
+        cudaFreeAsync(ws, s);
+        return st;
+      }
+    }
+    if (ev) cudaEventRecord(ev[1], s);
+
+    // ---- K5: bitmap pyramid (big levels one launch each, the rest in one CTA)
+    int l = lists ? L : 0;
+    while (l >= 1 && level_words(l - 1) > 4096) {
+      const int64_t nc = level_words(l - 1);
+      k_pyramid<<<(unsigned)ceil_div(2 * nc, 256), 256, 0, s>>>(
+          bmp + rp.word_off[l], bmp + rp.word_off[l - 1], bmp + rp.word_off[stride + l],
+          bmp + rp.word_off[stride + l - 1], nc);
+      ++launches;
+      --l;
+    }
+    if (l >= 1) {
+      PyramidTail pt{};
+      for (int k = 0; k <= L; ++k) {
+        pt.lvl[0][k] = bmp + rp.word_off[k];
+        pt.lvl[1][k] = bmp + rp.word_off[stride + k];
+        pt.nwords[k] = level_words(k);
+      }
+      pt.from_level = l;
+      k_pyramid_tail<<<1, 1024, 0, s>>>(pt);
+      ++launches;
+    }
+    // ---- rank directory, totals and per-level directory keys
+    rp.bmp = bmp;
+    rp.dir = dir;
+    rp.states = (uint64_t*)W(o_rst);
+    rp.tile_counter = tc + 9;
+    rp.totals = dplan->ktot;
+    uint64_t* lowkeys = (uint64_t*)W(o_lowkeys);
+    for (int set = 0; set < 2; ++set)
+      for (int k = 0; k <= L; ++k) {
+        uint64_t* dst = nullptr;
+        if (k < L) {
+          if (k == 0) dst = lowkeys + set * 9;
+          else if (k == 1) dst = lowkeys + set * 9 + 1;
+          else if (lists) dst = (uint64_t*)A(a_dir[set][k]);
+        }
+        rp.keys_out[set * stride + k] = dst;
+      }
+    if (lists) {
+      k_rank<<<(unsigned)rank_tiles, kRThreads, 0, s>>>(rp);
+      ++launches;
+    }
+    if (brun.scratch) {  // bucket path: bookmarks / non-empty keys at global box ranks
+      if (lists) {
+        HeadsParams hpar{};
+        for (int set = 0; set < 2; ++set) {
+          hpar.bmp[set] = bmp + rp.word_off[set * stride + L];
+          hpar.dir[set] = dir + rp.word_off[set * stride + L];
+        }
+        hpar.ktot_src = dplan->ktot + L;
+        hpar.ktot_recv = dplan->ktot + stride + L;
+        hpar.bstart = brun.bstart;
+        hpar.hpos = brun.hpos;
+        hpar.ne = ne_out;
+        hpar.bm = bm_out;
+        hpar.kinfo = dplan->kinfo;
+        k_bkt_heads<<<(unsigned)ceil_div(brun.g.nb, 8), 256, 0, s>>>(hpar, brun.g);
+        ++launches;
+      }
+      cudaFreeAsync(brun.scratch, s);
+    }
+    if (ev) cudaEventRecord(ev[2], s);
+
+    nwork_cap = 0;
+    if (lists) {
+      lp.level = L;
+      lp.ktot = dplan->ktot;
+      lp.bmp = bmp;
+      lp.dir = dir;
+      for (int set = 0; set < 2; ++set)
+        for (int k = 0; k <= L; ++k) lp.bmp_off[set][k] = rp.word_off[set * stride + k];
+      for (int k = 0; k < L; ++k) lp.rkeys[k] = rp.keys_out[stride + k];
+      lp.counts = (uint32_t*)W(o_cnt);
+      lp.bm[0] = (int64_t*)A(a_lbm[0]);
+      for (int k = 2; k <= L; ++k) lp.bm[k] = (int64_t*)A(a_lbm[k]);
+      for (int k = std::max(1, lists_lmin_host(L)); k <= L; ++k) nwork_cap += cap_level(m, k - 1);
+      if (L == 0) nwork_cap = 1;
+      const int lgrid = (int)std::max<int64_t>(
+          1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * 16));
+      ListsLayout* glay = (ListsLayout*)W(o_lay);
+      k_lists_plan<<<1, 32, 0, s>>>(lp, glay);
+      k_lists_count<<<lgrid, kLThreads, 0, s>>>(lp, glay);
+      k_lists_scan<<<(unsigned)std::max<int64_t>(1, scan_tiles_cap), kScanThreads, 0, s>>>(
+          lp, glay, (uint64_t*)W(o_lst), tc + 10, dplan->seg_totals);
+      launches += 3;
+    }
+    if (ev) cudaEventRecord(ev[3], s);
+
+    // ---- sizes back to the host (the build's single synchronisation)
+    cudaMemcpyAsync(hp, dplan, sizeof(BuildPlanHost), cudaMemcpyDeviceToHost, s);
+    cudaError_t ce = cudaStreamSynchronize(s);
+    if (ce != cudaSuccess) {
+      cudaFreeAsync(ws, s);
+      return fmmb_fail(h, FMMB_ERR_CUDA, "build phase A failed: %s", cudaGetErrorString(ce));
+    }
+    if (hp->fail && fast && attempt == 0) {  // a bucket overflowed: general sort
+      fast = false;
+      continue;
+    }
+    break;
   }
+  if (hp->fail) {
+    cudaFreeAsync(ws, s);
+    return fmmb_fail(h, FMMB_ERR_CUDA, "internal: bucket sort overflow after fallback");
+  }
+  h->last_sort_path = fast ? 1 : 2;
   if (hp->err) {
     cudaFreeAsync(ws, s);
     return fmmb_fail(h, FMMB_ERR_DOMAIN,
@@ -425,7 +594,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
         1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * 16));
     if (ev) cudaEventRecord(ev[4], s);
     k_lists_write<<<lgrid, kLThreads, 0, s>>>(lp, (const ListsLayout*)W(o_lay));
-    FMMB_LAUNCHED();
+    ++launches;
 
     out->neighbor_bookmark = lp.bm[0];
     out->neighbor_list = lp.ranks_out[0];
@@ -454,10 +623,9 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
   cudaFreeAsync(ws, s);
   out->n_launches = launches;
   h->launches = launches;
-  ce = cudaGetLastError();
+  cudaError_t ce = cudaGetLastError();
   if (ce != cudaSuccess)
     return fmmb_fail(h, FMMB_ERR_CUDA, "build launch failed: %s", cudaGetErrorString(ce));
-#undef FMMB_LAUNCHED
   return FMMB_OK;
 }
 

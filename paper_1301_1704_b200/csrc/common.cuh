@@ -68,6 +68,39 @@ __device__ __forceinline__ uint64_t encode_point(double x, double y, double z,
                  quantize_axis(z, level));
 }
 
+// 10-bit dilation in 32-bit arithmetic (levels <= 10: 3L <= 30 key bits).
+__device__ __forceinline__ uint32_t dilate3_10(uint32_t v) {
+  v = (v | (v << 16)) & 0x030000FFu;
+  v = (v | (v << 8)) & 0x0300F00Fu;
+  v = (v | (v << 4)) & 0x030C30C3u;
+  v = (v | (v << 2)) & 0x09249249u;
+  return v;
+}
+
+// encode_point for level <= 10 with a 32-bit fast path: when every scaled
+// coordinate t = x * 2^L lies in [0, 2^L) (the unit cube minus its upper
+// faces) truncation is a plain conversion; anything else (x = 1.0 clamps,
+// negative / NaN / huge inputs) takes the exact reference path.  Returns the
+// same 64-bit key as encode_point.
+__device__ __forceinline__ uint64_t encode_point_narrow(double x, double y, double z,
+                                                        int level, double grid) {
+  const double tx = __dmul_rn(x, grid), ty = __dmul_rn(y, grid), tz = __dmul_rn(z, grid);
+  if (tx >= 0.0 && tx < grid && ty >= 0.0 && ty < grid && tz >= 0.0 && tz < grid) {
+    const uint32_t ix = __double2uint_rz(tx), iy = __double2uint_rz(ty),
+                   iz = __double2uint_rz(tz);
+    return dilate3_10(ix) | (dilate3_10(iy) << 1) | (dilate3_10(iz) << 2);
+  }
+  return encode_point(x, y, z, level);
+}
+
+// level-generic entry: NARROW selects the 32-bit fast path (level <= 10)
+template <bool NARROW>
+__device__ __forceinline__ uint64_t encode_any(double x, double y, double z, int level,
+                                               double grid) {
+  if (NARROW) return encode_point_narrow(x, y, z, level, grid);
+  return encode_point(x, y, z, level);
+}
+
 // ------------------------------------------------- decoupled look-back ----
 // 64-bit tile state: [63:62] status, [61:0] value (Merrill & Garland 2016).
 constexpr uint64_t kStInvalid = 0ull;

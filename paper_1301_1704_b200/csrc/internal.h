@@ -11,6 +11,8 @@ struct fmmb_handle_s {
   int num_sms = 148;
   void* pinned = nullptr;  // small pinned block for size read-back
   int64_t launches = 0;
+  int sort_path = 0;       // 0 auto (bucket sort, Onesweep on overflow), 1 bucket, 2 Onesweep
+  int last_sort_path = 0;  // path the last build's sort phase completed on
   std::string err;
 };
 

@@ -134,6 +134,7 @@ class FmmStructures:
     stencils: TranslationStencils
     build_seconds: dict = field(default_factory=dict)
     n_launches: int = 0
+    sort_path: str = ""  # "bucket" | "onesweep": strategy the sort phase completed on
 
     def to_numpy(self) -> "FmmStructures":
         """Host copy in the reference's numpy layout (one sync)."""
@@ -173,6 +174,7 @@ class FmmStructures:
                                          {l: npy(v) for l, v in sc.items()}),
             build_seconds=self.build_seconds,
             n_launches=self.n_launches,
+            sort_path=self.sort_path,
         )
 
 
@@ -235,7 +237,9 @@ def build_all_device(src: torch.Tensor, charges: torch.Tensor | None, recv: torc
     if alloc.error is not None:
         raise alloc.error
     _lib.check(st, h)
-    return _structures_from_c(out, alloc, charges is not None, events)
+    res = _structures_from_c(out, alloc, charges is not None, events)
+    res.sort_path = _lib.SORT_PATHS.get(int(lib.fmmb_last_sort_path(h)), "")
+    return res
 
 
 def build_all(

@@ -30,8 +30,16 @@ CASES = [
 ]
 
 
+@pytest.fixture(params=["auto", "onesweep"])
+def sort_path(request, gpu):
+    """Both sort-phase strategies (bucket sort with overflow rerun, Onesweep)."""
+    gpu._lib.set_sort_path(request.param)
+    yield request.param
+    gpu._lib.set_sort_path("auto")
+
+
 @pytest.mark.parametrize("n,m,level,dist,seed", CASES)
-def test_build_all_matches_reference(gpu, ref, n, m, level, dist, seed):
+def test_build_all_matches_reference(gpu, ref, sort_path, n, m, level, dist, seed):
     src, q, _ = generate(n, 1, dist, seed)
     _, _, recv = generate(1, m, dist, seed + 1000)
     budget = max(2 << 30, 8 ** level * 8)
@@ -39,6 +47,42 @@ def test_build_all_matches_reference(gpu, ref, n, m, level, dist, seed):
     got = gpu.build_all(src, q, recv, max_level=level, histogram_budget_bytes=budget)
     errors = compare_structures(got, want)
     assert not errors, "\n".join(errors)
+    if sort_path == "onesweep" and n + m > 0 and gpu.lists._bitmap_path_ok(level, n + m):
+        assert got.sort_path == "onesweep"
+
+
+def test_bucket_overflow_reruns_on_onesweep(gpu, ref):
+    """A dense cluster overflows the bucket sort's shared-memory capacity: the
+    build reruns on the Onesweep path and still matches the reference."""
+    rng = np.random.default_rng(5)
+    src = 0.3 + 1e-4 * rng.random((60000, 3))  # one finest box at L=5
+    recv = rng.random((5000, 3))
+    q = rng.normal(size=60000)
+    want = ref.build_all(src, q, recv, max_level=5)
+    got = gpu.build_all(src, q, recv, max_level=5)
+    assert got.sort_path == "onesweep"
+    assert not compare_structures(got, want)
+
+
+def test_crowded_box_inside_bucket(gpu, ref):
+    """A box with more points than the in-box ranking handles (> 64) inside a
+    bucket that still fits shared memory: the bucket falls back to the
+    in-smem LSD passes; the rest of the build stays on the bucket path."""
+    src, q, recv = generate(2**16, 2**16, "uniform", 31)
+    src = np.concatenate([src, np.repeat(src[:1], 200, axis=0)])
+    q = np.concatenate([q, np.arange(200.0)])
+    want = ref.build_all(src, q, recv, max_level=5)
+    got = gpu.build_all(src, q, recv, max_level=5)
+    assert got.sort_path == "bucket"
+    assert not compare_structures(got, want)
+
+
+def test_uniform_build_takes_bucket_path(gpu, ref):
+    src, q, recv = generate(2**17, 2**17, "uniform", 21)
+    want = ref.build_all(src, q, recv, max_level=6)
+    got = gpu.build_all(src, q, recv, max_level=6)
+    assert got.sort_path == "bucket"
+    assert not compare_structures(got, want)
 
 
 def test_build_all_receivers_without_charges(gpu, ref):
