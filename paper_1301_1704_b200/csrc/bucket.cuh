@@ -11,20 +11,20 @@
 //                      shared memory, one row per CTA.
 //   S  k_bkt_scan    : column sums, exclusive scan -> bucket starts; the
 //                      starts seed one global cursor per bucket.
-//   S  k_bkt_scatter : read xyz(+q) again; each warp owns a contiguous input
-//                      RANGE and moves its points, as 32-byte records
-//                      {x, y, z, q | recv index}, to its buckets' cursors
-//                      (warp-aggregated atomics).  Cursors advance in time, so
-//                      every bucket fills front to back and L2 merges the
-//                      partial lines; the order inside a bucket is by range
-//                      chunk, not by input index.
+//   S  k_bkt_scatter : read xyz(+q) again, streamed through a shared-memory
+//                      ring by TMA bulk copies; every point claims a slot at
+//                      its bucket's cursor (one atomic per point) and is
+//                      written there as a 32-byte record {x, y, z, q | recv
+//                      index} (+ its source index).  Cursors advance in time,
+//                      so every bucket fills front to back and L2 merges the
+//                      partial lines; the order inside a bucket is arbitrary.
 //   L  k_bkt_local   : one CTA per bucket: TMA bulk copy of the bucket's
-//                      records into shared memory, stable LSD sort of the
-//                      composite (low key bits, range id) -- the range id
-//                      restores input order, since a range's chunks land in
-//                      its input order -- then the reference layout (points,
-//                      charges, permutation, boxes) with box heads giving the
-//                      bookmarks, non-empty keys and level-L occupancy bits.
+//                      records into shared memory, then a sort by (low key
+//                      bits, combined input index) -- the index makes the
+//                      order the stable one whatever the arrival order was --
+//                      and the reference layout (points, charges,
+//                      permutation, boxes); box heads give the bookmarks,
+//                      non-empty keys and level-L occupancy bits.
 //
 // DRAM bytes per point (src / recv): H 24/24, S 32+36 / 24+32, L 36+48 / 32+40.
 //
@@ -40,12 +40,10 @@ namespace fmmb {
 
 constexpr int kBucketBitsMax = 14;  // <= 2^14 buckets per set
 constexpr int kBucketAvg = 1024;    // bb chosen so the mean bucket is <= this
-constexpr int kWidBitsMax = 11;     // <= 2048 scatter ranges
 constexpr int kHThreads = 512;      // H pass
 constexpr int kHItems = 8;          // rows per lane per step (memory-level parallelism)
 constexpr int kHChunk = 32 * kHItems;
-constexpr int kSItems = 4;          // S pass: rows per lane per step (double-buffered)
-constexpr int kSChunk = 32 * kSItems;
+
 constexpr int kScanBuckets = 1024;  // buckets per CTA of the scan
 constexpr int kCursorStride = 32;   // u32 words per bucket cursor: one 128-B line each, so
                                     // the scatter's cursor atomics never share an L2 line
@@ -56,11 +54,8 @@ struct BucketGeo {
   int shift;      // 3L - bb: low key bits sorted inside a bucket
   int nb;         // 2 << bb buckets
   int64_t n, m;   // sources, receivers
-  int rbits;      // input points per scatter range = 2^rbits (>= kSChunk)
-  int nranges;
-  int wbits;      // bits of a range id
+  int cbits;      // bits of a combined input index (n + m <= 2^cbits)
   int hgrid;      // CTAs (histogram rows) of the H pass
-  int swarps;     // warps per CTA of the S pass
 };
 
 __host__ inline int ceil_log2(int64_t v) {
@@ -82,14 +77,7 @@ __host__ inline BucketGeo bucket_geo(int level, int64_t n, int64_t m, int num_sm
   g.n = n;
   g.m = m;
   const int64_t tot = n + m;
-  int rb = ceil_log2((tot + (1 << kWidBitsMax) - 1) >> kWidBitsMax);
-  if ((1 << rb) < kSChunk) rb = ceil_log2(kSChunk);
-  g.rbits = rb;
-  g.nranges = (int)((tot + (1ll << rb) - 1) >> rb);
-  if (g.nranges < 1) g.nranges = 1;
-  g.wbits = ceil_log2(g.nranges);
-  g.swarps = (g.nranges + num_sms - 1) / num_sms;
-  if (g.swarps > 16) g.swarps = 16;
+  g.cbits = ceil_log2(tot > 1 ? tot : 2);
   const int64_t hchunks = (tot + (int64_t)kHThreads * kHItems - 1) / ((int64_t)kHThreads * kHItems);
   g.hgrid = (int)(hchunks < num_sms ? (hchunks < 1 ? 1 : hchunks) : num_sms);
   return g;
@@ -255,138 +243,133 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// S pass.  Each warp streams its range in chunks of kSRows rows through a
-// kSStages-deep shared-memory ring filled by TMA bulk copies (one elected
-// lane; chunks that straddle the src/recv boundary, end the range early or
-// are not 16-byte aligned are loaded by the warp instead).  Chunk c+1's
-// cursor atomics are in flight while chunk c is stored, and chunks c+1, c+2
-// are in flight from HBM, so neither round trip is exposed.
-constexpr int kSRows = 128;
-constexpr int kSStages = 3;
+// S pass.  One persistent CTA per SM streams a contiguous input range
+// through a kSStages-deep shared-memory ring of kSRows-row stages filled by
+// TMA bulk copies (thread 0 produces).  Thread t owns row t of every stage:
+// it claims the row's bucket slot with one atomic, and stores the record
+// kSDepth stages later straight from the ring, so the atomic round trip
+// overlaps the following stages and the payload never sits in registers;
+// the stage is released (`empty` mbarrier) after that store.  Stages that
+// straddle the src/recv boundary or are not 16-byte aligned are filled by
+// their consumers with plain loads instead.
+constexpr int kSThreads = 1024;
+constexpr int kSRows = kSThreads;   // one row per thread per stage
+constexpr int kSStages = 6;
+constexpr int kSLead = 3;           // stages in flight ahead of the claim
+constexpr int kSDepth = 2;          // stages between claim and store
+static_assert(kSLead + kSDepth + 1 <= kSStages, "ring too small");
 constexpr int kSStageBytes = kSRows * 32;  // xyz (24 B) + q (8 B) per row
-constexpr int kSMaxWarps = 16;
 
-__host__ inline size_t scatter_smem_bytes(int warps) {
-  return (size_t)warps * kSStages * (kSStageBytes + 8);
+__host__ __device__ constexpr size_t scatter_smem_bytes() {
+  return (size_t)kSStages * kSStageBytes + 2 * kSStages * 8;
+}
+
+__host__ inline int64_t scatter_rows_per_cta(int64_t tot, int grid) {
+  int64_t r = (tot + grid - 1) / grid;
+  return ((r + kSRows - 1) / kSRows) * kSRows;
 }
 
 template <bool NARROW>
-__global__ void __launch_bounds__(kSMaxWarps * 32)
+__global__ void __launch_bounds__(kSThreads, 1)
     k_bkt_scatter(const double* __restrict__ src, const double* __restrict__ q,
                   const double* __restrict__ recv, const BucketGeo g, int level,
-                  uint32_t* __restrict__ cursor, double* __restrict__ rec,
+                  int64_t cta_rows, uint32_t* __restrict__ cursor, double* __restrict__ rec,
                   uint32_t* __restrict__ idx) {
   extern __shared__ __align__(128) unsigned char sc_smem[];
-  constexpr int kItems = kSRows / 32;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int r = blockIdx.x * g.swarps + warp;
-  if (r >= g.nranges) return;  // warp-uniform; no block barriers below
-  double* stage0 = reinterpret_cast<double*>(sc_smem) + (size_t)warp * kSStages * (kSStageBytes / 8);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sc_smem + (size_t)g.swarps * kSStages * kSStageBytes) +
-                   warp * kSStages;
-  if (lane == 0) {
-    for (int st = 0; st < kSStages; ++st) mbar_init(bars + st);
+  uint64_t* full = reinterpret_cast<uint64_t*>(sc_smem + (size_t)kSStages * kSStageBytes);
+  uint64_t* empty = full + kSStages;
+  const int tid = threadIdx.x;
+  const int64_t n = g.n, tot = n + g.m;
+  const int64_t lo = (int64_t)blockIdx.x * cta_rows;
+  const int64_t hi = lo + cta_rows < tot ? lo + cta_rows : tot;
+  if (lo >= hi) return;  // block-uniform
+  const int nst = (int)((hi - lo + kSRows - 1) / kSRows);
+  if (tid == 0) {
+    for (int st = 0; st < kSStages; ++st) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(full + st)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(empty + st)),
+                   "r"(kSThreads));
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  __syncwarp();
-  const int64_t n = g.n, tot = n + g.m;
-  const int64_t lo = (int64_t)r << g.rbits;
-  const int64_t hi = lo + (1ll << g.rbits) < tot ? lo + (1ll << g.rbits) : tot;
-  const int nchunks = (int)((hi - lo + kSRows - 1) / kSRows);
+  __syncthreads();
   const uint64_t kmask = (1ull << g.sbits) - 1ull;
   const double grid = (double)(1ll << level);
-  const unsigned lt = lanemask_lt();
-
-  auto issue = [&](int c) {  // fill stage c % kSStages with chunk c
-    const int st = c % kSStages;
-    double* xyz = stage0 + (size_t)st * (kSStageBytes / 8);
-    double* qs = xyz + 3 * kSRows;
-    const int64_t base = lo + (int64_t)c * kSRows;
-    const int rows = (int)(hi - base < kSRows ? hi - base : kSRows);
+  auto stage_xyz = [&](int k) {
+    return reinterpret_cast<double*>(sc_smem + (size_t)(k % kSStages) * kSStageBytes);
+  };
+  auto stage_rows = [&](int k) {
+    const int64_t base = lo + (int64_t)k * kSRows;
+    return (int)(hi - base < kSRows ? hi - base : kSRows);
+  };
+  auto stage_tma = [&](int k) {
+    const int64_t base = lo + (int64_t)k * kSRows;
+    const int rows = stage_rows(k);
     const bool is_src = base < n;
+    if (is_src && base + rows > n) return false;  // straddles src | recv
     const double* rp = row_ptr(src, recv, n, base);
-    const bool tma = rows == kSRows && (base + kSRows <= n || base >= n) &&
-                     ((uintptr_t)rp & 15) == 0 &&
-                     (!is_src || !q || ((uintptr_t)(q + base) & 15) == 0);
-    __syncwarp();  // every lane is done reading this stage (chunk c - kSStages)
-    if (tma) {
-      if (lane == 0) {
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        const uint32_t qbytes = (is_src && q) ? kSRows * 8 : 0;
-        mbar_expect_tx(bars + st, kSRows * 24 + qbytes);
-        bulk_g2s(xyz, rp, kSRows * 24, bars + st);
-        if (qbytes) bulk_g2s(qs, q + base, qbytes, bars + st);
-      }
+    if (((uintptr_t)rp & 15) || ((rows * 24) & 15)) return false;
+    if (is_src && q && (((uintptr_t)(q + base) & 15) || ((rows * 8) & 15))) return false;
+    return true;
+  };
+  auto produce = [&](int k) {  // thread 0 only
+    const int st = k % kSStages;
+    if (k >= kSStages) mbar_wait(empty + st, (uint32_t)(k / kSStages - 1) & 1u);
+    if (stage_tma(k)) {
+      const int64_t base = lo + (int64_t)k * kSRows;
+      const int rows = stage_rows(k);
+      double* xyz = stage_xyz(k);
+      const bool with_q = base < n && q;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(full + st, rows * 24 + (with_q ? rows * 8 : 0));
+      bulk_g2s(xyz, row_ptr(src, recv, n, base), rows * 24, full + st);
+      if (with_q) bulk_g2s(xyz + 3 * kSRows, q + base, rows * 8, full + st);
     } else {
-      for (int k = 0; k < kItems; ++k) {
-        const int row = k * 32 + lane;
-        const int64_t i = base + row;
-        if (row < rows) {
-          const double* p = row_ptr(src, recv, n, i);
-          xyz[3 * row] = __ldg(p);
-          xyz[3 * row + 1] = __ldg(p + 1);
-          xyz[3 * row + 2] = __ldg(p + 2);
-          if (i < n) qs[row] = q ? __ldg(q + i) : 0.0;
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bars + st);
+      mbar_arrive(full + st);  // consumers fill this stage themselves
     }
   };
-  auto wait = [&](int c) { mbar_wait(bars + c % kSStages, (uint32_t)(c / kSStages) & 1u); };
-  auto claim = [&](int c, unsigned (&pe)[kItems], uint32_t (&cu)[kItems]) {
-    const double* xyz = stage0 + (size_t)(c % kSStages) * (kSStageBytes / 8);
-    const int64_t base = lo + (int64_t)c * kSRows;
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-      const int row = k * 32 + lane;
-      const int64_t i = base + row;
-      uint32_t b = 0xFFFFFFFFu;
-      if (i < hi)
-        b = bucket_of(encode_any<NARROW>(xyz[3 * row], xyz[3 * row + 1], xyz[3 * row + 2],
-                                         level, grid) &
-                          kmask,
-                      i >= n, g);
-      pe[k] = __match_any_sync(0xffffffffu, b);
-      cu[k] = 0;
-      if (i < hi && lane == __ffs(pe[k]) - 1)
-        cu[k] = atomicAdd(cursor + (size_t)b * kCursorStride, __popc(pe[k]));
+  // claim: wait for the stage, (fill it if it is a plain-load stage), slot atomic
+  auto claim = [&](int k) -> uint32_t {
+    const int st = k % kSStages;
+    mbar_wait(full + st, (uint32_t)(k / kSStages) & 1u);
+    double* xyz = stage_xyz(k);
+    const int64_t i = lo + (int64_t)k * kSRows + tid;
+    if (tid >= stage_rows(k)) return 0;
+    if (!stage_tma(k)) {  // row-private fill: only this thread reads the row
+      const double* p = row_ptr(src, recv, n, i);
+      xyz[3 * tid] = __ldg(p);
+      xyz[3 * tid + 1] = __ldg(p + 1);
+      xyz[3 * tid + 2] = __ldg(p + 2);
+      if (i < n) xyz[3 * kSRows + tid] = q ? __ldg(q + i) : 0.0;
     }
+    const uint32_t b = bucket_of(
+        encode_any<NARROW>(xyz[3 * tid], xyz[3 * tid + 1], xyz[3 * tid + 2], level, grid) & kmask,
+        i >= n, g);
+    return atomicAdd(cursor + (size_t)b * kCursorStride, 1u);
   };
-  auto store = [&](int c, const unsigned (&pe)[kItems], const uint32_t (&cu)[kItems]) {
-    const double* xyz = stage0 + (size_t)(c % kSStages) * (kSStageBytes / 8);
-    const double* qs = xyz + 3 * kSRows;
-    const int64_t base = lo + (int64_t)c * kSRows;
-#pragma unroll
-    for (int k = 0; k < kItems; ++k) {
-      const int row = k * 32 + lane;
-      const int64_t i = base + row;
-      const uint32_t before = __shfl_sync(0xffffffffu, cu[k], __ffs(pe[k]) - 1);
-      if (i < hi) {
-        const uint32_t dst = before + __popc(pe[k] & lt);
-        const double w = i < n ? (q ? qs[row] : 0.0) : __longlong_as_double(i - n);
-        st_v4f64(rec + 4 * (size_t)dst, xyz[3 * row], xyz[3 * row + 1], xyz[3 * row + 2], w);
-        if (i < n) idx[dst] = (uint32_t)i;
-      }
+  auto store = [&](int k, uint32_t dst) {
+    const double* xyz = stage_xyz(k);
+    const int64_t i = lo + (int64_t)k * kSRows + tid;
+    if (tid < stage_rows(k)) {
+      const double w = i < n ? (q ? xyz[3 * kSRows + tid] : 0.0) : __longlong_as_double(i - n);
+      st_v4f64(rec + 4 * (size_t)dst, xyz[3 * tid], xyz[3 * tid + 1], xyz[3 * tid + 2], w);
+      if (i < n) idx[dst] = (uint32_t)i;
     }
+    mbar_arrive(empty + k % kSStages);
   };
-  unsigned pa[kItems], pb[kItems];
-  uint32_t ua[kItems], ub[kItems];
-  auto step = [&](int c, const unsigned (&pc)[kItems], const uint32_t (&uc)[kItems],
-                  unsigned (&pn)[kItems], uint32_t (&un)[kItems]) {
-    if (c + kSStages - 1 < nchunks) issue(c + kSStages - 1);
-    if (c + 1 < nchunks) {
-      wait(c + 1);
-      claim(c + 1, pn, un);
-    }
-    store(c, pc, uc);
+  if (tid == 0)
+    for (int k = 0; k < kSLead && k < nst; ++k) produce(k);
+  uint32_t d0 = 0, d1 = 0, d2 = 0;
+  // step k: produce k+lead, claim k, store k-2 (slots rotate through d0, d1, d2)
+  auto step = [&](int k, uint32_t& dk, uint32_t dold) {
+    if (tid == 0 && k + kSLead < nst) produce(k + kSLead);
+    if (k < nst) dk = claim(k);
+    if (k >= kSDepth && k - kSDepth < nst) store(k - kSDepth, dold);
   };
-  for (int c = 0; c < kSStages - 1 && c < nchunks; ++c) issue(c);
-  wait(0);
-  claim(0, pa, ua);
-  for (int c = 0; c < nchunks; c += 2) {  // unrolled by two: static register buffers
-    step(c, pa, ua, pb, ub);
-    if (c + 1 < nchunks) step(c + 1, pb, ub, pa, ua);
+  for (int k = 0; k < nst + kSDepth; k += 3) {  // unrolled by three: static slot registers
+    step(k, d0, d1);
+    step(k + 1, d1, d2);
+    step(k + 2, d2, d0);
   }
 }
 
@@ -491,8 +474,7 @@ struct LocalOut {
 // per-box counts (shared atomics), unstable placement into box segments and a
 // rank of each point among its box's points by combined input index (boxes
 // hold a handful of points; a box of more than 64 falls back).  Otherwise a
-// stable LSD sort of the composite (low key bits, range id): a range's chunks
-// land in its input order, so range id then arrival order is input order.
+// LSD sort of the composite (low key bits, combined input index).
 //
 // HEADS: box heads go to the occupancy bitmap plus a bucket-local list of
 // head positions (hpos[bs + h]); k_bkt_heads later writes bookmarks and
@@ -580,7 +562,7 @@ __global__ void __launch_bounds__(kLcThreads)
       s_idx[j] = ci;
       atomicAdd(&s_wh[lk], 1u);
     } else {
-      k0[j] = ((CK)(key & lmask) << g.wbits) | (CK)(ci >> g.rbits);
+      k0[j] = ((CK)(key & lmask) << g.cbits) | (CK)ci;
     }
     p0[j] = (uint16_t)j;
   }
@@ -635,7 +617,7 @@ __global__ void __launch_bounds__(kLcThreads)
     __syncthreads();
     if (!ranked) {  // a crowded box: fall back to the LSD passes below
       for (int j = tid; j < B; j += kLcThreads)
-        k0[j] = ((CK)k0[j] << g.wbits) | (CK)(s_idx[j] >> g.rbits);
+        k0[j] = ((CK)k0[j] << g.cbits) | (CK)s_idx[j];
       __syncthreads();
     }
   }
@@ -680,10 +662,10 @@ __global__ void __launch_bounds__(kLcThreads)
     }
     return;
   }
-  // phase 2: stable LSD passes (range id first, then the key bits)
+  // phase 2: LSD passes over the composite (index bits first, then key bits)
   CK* kc = k0;
   uint16_t* pc = p0;
-  const int cbits = g.shift + g.wbits;
+  const int cbits = g.shift + g.cbits;
   for (int ds = 0; ds < cbits; ds += kLcDigit) {
     const int db = cbits - ds < kLcDigit ? cbits - ds : kLcDigit;
     CK* ko = kc == k0 ? k1 : k0;
@@ -692,7 +674,7 @@ __global__ void __launch_bounds__(kLcThreads)
     kc = ko;
     pc = po;
   }
-  const int wb = g.wbits;
+  const int wb = g.cbits;
   int64_t hbase = 0;
   if (!HEADS) {
     // phase 3: head count, box-rank base by look-back over buckets

@@ -82,9 +82,9 @@ extern "C" fmmb_status fmmb_create(int device, fmmb_handle_t* out) {
   cudaFuncSetAttribute(k_bkt_hist<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (2 << kBucketBitsMax) * (int)sizeof(uint32_t));
   cudaFuncSetAttribute(k_bkt_scatter<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)scatter_smem_bytes(kSMaxWarps));
+                       (int)scatter_smem_bytes());
   cudaFuncSetAttribute(k_bkt_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)scatter_smem_bytes(kSMaxWarps));
+                       (int)scatter_smem_bytes());
 #define FMMB_LCATTR(CK, NW, HD)                                                        \
   cudaFuncSetAttribute(k_bkt_local<CK, NW, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                        (int)lc_smem_bytes<CK>())
@@ -195,14 +195,15 @@ void launch_local(const double* rec, uint32_t* idx, const uint32_t* bstart, cons
 
 template <bool NARROW>
 void launch_hs(const double* src, const double* q, const double* recv, const BucketGeo& g,
-               int L, uint32_t* mat, uint32_t* bstart, uint32_t* cursor, uint64_t* sst,
+               int num_sms, int L, uint32_t* mat, uint32_t* bstart, uint32_t* cursor, uint64_t* sst,
                uint32_t* ctl, double* rec, uint32_t* idx, uint32_t* err, cudaStream_t s) {
   k_bkt_hist<NARROW><<<(unsigned)g.hgrid, kHThreads, (size_t)g.nb * 4, s>>>(src, recv, g, L,
                                                                              mat, err);
   k_bkt_scan<<<(unsigned)ceil_div(g.nb, kScanBuckets), 256, 0, s>>>(mat, g, bstart, cursor, sst,
                                                                     ctl + 0, ctl + 2);
-  k_bkt_scatter<NARROW><<<(unsigned)ceil_div(g.nranges, g.swarps), (unsigned)g.swarps * 32,
-                          scatter_smem_bytes(g.swarps), s>>>(src, q, recv, g, L, cursor, rec, idx);
+  const int sgrid = (int)std::min<int64_t>(num_sms, ceil_div(g.n + g.m, kSRows));
+  k_bkt_scatter<NARROW><<<(unsigned)sgrid, kSThreads, scatter_smem_bytes(), s>>>(
+      src, q, recv, g, L, scatter_rows_per_cta(g.n + g.m, sgrid), cursor, rec, idx);
 }
 
 fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int64_t n,
@@ -235,10 +236,10 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
   uint64_t* lst = (uint64_t*)(w + o_lst);
   const bool narrow = L <= 10;
   if (narrow)
-    launch_hs<true>(src, q, recv, g, L, mat, bstart, cursor, sst, ctl, rec, idx, &dplan->err, s);
+    launch_hs<true>(src, q, recv, g, h->num_sms, L, mat, bstart, cursor, sst, ctl, rec, idx, &dplan->err, s);
   else
-    launch_hs<false>(src, q, recv, g, L, mat, bstart, cursor, sst, ctl, rec, idx, &dplan->err, s);
-  const bool ck32 = g.shift + g.wbits <= 32;
+    launch_hs<false>(src, q, recv, g, h->num_sms, L, mat, bstart, cursor, sst, ctl, rec, idx, &dplan->err, s);
+  const bool ck32 = g.shift + g.cbits <= 32;
 #define FMMB_LOCAL(CK, NW, HD) \
   launch_local<CK, NW, HD>(rec, idx, bstart, g, L, o, lst, ctl, &dplan->fail, s)
   if (heads) {

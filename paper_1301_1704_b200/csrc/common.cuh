@@ -86,8 +86,12 @@ __device__ __forceinline__ uint64_t encode_point_narrow(double x, double y, doub
                                                         int level, double grid) {
   const double tx = __dmul_rn(x, grid), ty = __dmul_rn(y, grid), tz = __dmul_rn(z, grid);
   if (tx >= 0.0 && tx < grid && ty >= 0.0 && ty < grid && tz >= 0.0 && tz < grid) {
-    const uint32_t ix = __double2uint_rz(tx), iy = __double2uint_rz(ty),
-                   iz = __double2uint_rz(tz);
+    // floor(t) for 0 <= t < 2^31 without the (XU-pipe) F2I conversion:
+    // 2^52 + t rounded toward zero is 2^52 + floor(t); its low word is floor(t)
+    constexpr double kMagic = 4503599627370496.0;  // 2^52
+    const uint32_t ix = (uint32_t)__double2loint(__dadd_rz(tx, kMagic)),
+                   iy = (uint32_t)__double2loint(__dadd_rz(ty, kMagic)),
+                   iz = (uint32_t)__double2loint(__dadd_rz(tz, kMagic));
     return dilate3_10(ix) | (dilate3_10(iy) << 1) | (dilate3_10(iz) << 2);
   }
   return encode_point(x, y, z, level);
