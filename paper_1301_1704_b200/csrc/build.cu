@@ -336,27 +336,21 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
   rp.tile_off[rp.nseg] = tiles;
   const int64_t bmp_words = lists ? words : 0, rank_tiles = lists ? tiles : 0;
 
-  // list count segments: capacity from min(m, 8^l)
-  int64_t cnt_cap = 0;
-  for (int sg = 0; sg <= kMaxLevel; ++sg) {
-    int64_t len = 0;
-    if (sg == 0) len = cap_level(m, L) + 1;
-    else if (sg >= 2 && sg <= L) len = cap_level(m, sg) + 1;
-    cnt_cap += round_up(len, kScanTile);
-  }
-  const int64_t scan_tiles_cap = cnt_cap / kScanTile;
-
+  // count-scan tiles: capacity from min(m, 8^(l-1)) receiver parents per level
+  int64_t cs_tiles = 1;
+  for (int l = std::max(1, lists_lmin_host(L)); l <= L; ++l)
+    cs_tiles += ceil_div(cap_level(m, l - 1), kCsParents);
   // ---- workspace: [zeroed control | rest]
   Carver z;
   const size_t o_tc = z.take<uint32_t>(16);  // tile counters
   const size_t o_rst = z.take<uint64_t>(rank_tiles);
-  const size_t o_lst = z.take<uint64_t>(scan_tiles_cap);
+  const size_t o_st4 = z.take<uint64_t>(lists ? cs_tiles : 0);
+  const size_t o_st2 = z.take<uint64_t>(lists ? cs_tiles : 0);
   const size_t o_plan = z.take<BuildPlanHost>(1);
   const size_t o_bmp = z.take<uint64_t>(bmp_words);
   const size_t zero_bytes = z.off;
   const size_t o_dir = z.take<uint32_t>(bmp_words);
   const size_t o_lowkeys = z.take<uint64_t>(2 * (1 + 8));  // levels 0,1 keys
-  const size_t o_cnt = z.take<uint32_t>(cnt_cap);
   const size_t o_lay = z.take<ListsLayout>(1);
 
   char* ws = nullptr;
@@ -502,7 +496,6 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
       for (int set = 0; set < 2; ++set)
         for (int k = 0; k <= L; ++k) lp.bmp_off[set][k] = rp.word_off[set * stride + k];
       for (int k = 0; k < L; ++k) lp.rkeys[k] = rp.keys_out[stride + k];
-      lp.counts = (uint32_t*)W(o_cnt);
       lp.bm[0] = (int64_t*)A(a_lbm[0]);
       for (int k = 2; k <= L; ++k) lp.bm[k] = (int64_t*)A(a_lbm[k]);
       for (int k = std::max(1, lists_lmin_host(L)); k <= L; ++k) nwork_cap += cap_level(m, k - 1);
@@ -511,10 +504,9 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
           1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * 16));
       ListsLayout* glay = (ListsLayout*)W(o_lay);
       k_lists_plan<<<1, 32, 0, s>>>(lp, glay);
-      k_lists_count<<<lgrid, kLThreads, 0, s>>>(lp, glay);
-      k_lists_scan<<<(unsigned)std::max<int64_t>(1, scan_tiles_cap), kScanThreads, 0, s>>>(
-          lp, glay, (uint64_t*)W(o_lst), tc + 10, dplan->seg_totals);
-      launches += 3;
+      k_lists_cscan<<<(unsigned)cs_tiles, kLThreads, 0, s>>>(
+          lp, glay, (uint64_t*)W(o_st4), (uint64_t*)W(o_st2), tc + 10, dplan->seg_totals);
+      launches += 2;
     }
     if (ev) cudaEventRecord(ev[3], s);
 

@@ -23,9 +23,6 @@ namespace fmmb {
 
 constexpr int kLThreads = 256;
 constexpr int kLWarps = kLThreads / 32;
-constexpr int kScanThreads = 256;
-constexpr int kScanItems = 8;
-constexpr int kScanTile = kScanThreads * kScanItems;  // 2048 counts
 
 // Segment ids of the count/bookmark arrays: 0 = E2 at max level, l = E4 at l.
 struct ListsParams {
@@ -35,7 +32,6 @@ struct ListsParams {
   const uint32_t* dir;       // rank directories, same layout
   int64_t bmp_off[2][kMaxLevel + 1];
   const uint64_t* rkeys[kMaxLevel + 1];  // receiver box keys per level < L
-  uint32_t* counts;          // padded segments (count pass output)
   int64_t* bm[kMaxLevel + 1];            // bookmark arrays per segment
   int64_t* ranks_out[kMaxLevel + 1];     // write pass: [0]=E2 list, [l]=E4 ranks
   int16_t* codes_out[kMaxLevel + 1];     // [l]=E4 codes
@@ -46,9 +42,10 @@ struct ListsParams {
 struct ListsLayout {
   int lmin;                     // first level with work
   int64_t work_off[kMaxLevel + 2];  // prefix of receiver-parent counts
-  int64_t seg_len[kMaxLevel + 1];
-  int64_t seg_off[kMaxLevel + 2];
+  int64_t tile_off[kMaxLevel + 2];  // prefix of count-scan tiles per level
 };
+
+constexpr int kCsParents = 64;  // receiver parents per count-scan tile (8 per warp)
 
 __device__ __forceinline__ int lists_lmin(int L) { return L >= 2 ? 2 : L; }
 
@@ -56,23 +53,23 @@ __device__ inline void lists_layout(const ListsParams& p, ListsLayout& lay) {
   const int L = p.level;
   const int stride = L + 1;
   lay.lmin = lists_lmin(L);
-  int64_t w = 0;
-  for (int l = 0; l <= kMaxLevel + 1; ++l) lay.work_off[l] = 0;
+  int64_t w = 0, t = 0;
+  for (int l = 0; l <= kMaxLevel + 1; ++l) lay.work_off[l] = lay.tile_off[l] = 0;
   for (int l = 0; l <= L; ++l) {
     lay.work_off[l] = w;
-    if (l >= lay.lmin) w += (l == 0) ? p.ktot[stride + 0] : p.ktot[stride + l - 1];
+    lay.tile_off[l] = t;
+    if (l >= lay.lmin) {
+      const int64_t np = (l == 0) ? p.ktot[stride + 0] : p.ktot[stride + l - 1];
+      w += np;
+      t += (np + kCsParents - 1) / kCsParents;
+    }
   }
   lay.work_off[L + 1] = w;
-  int64_t off = 0;
-  for (int s = 0; s <= kMaxLevel; ++s) {
-    int64_t len = 0;
-    if (s == 0) len = p.ktot[stride + L] + 1;
-    else if (s >= 2 && s <= L) len = p.ktot[stride + s] + 1;
-    lay.seg_len[s] = len;
-    lay.seg_off[s] = off;
-    off += round_up(len, kScanTile);
-  }
-  lay.seg_off[kMaxLevel + 1] = off;
+  lay.tile_off[L + 1] = t;
+}
+
+__device__ __forceinline__ uint32_t children_mask(const uint64_t* bmp, uint64_t p) {
+  return (uint32_t)(__ldg(bmp + (p >> 3)) >> ((int)(p & 7) * 8)) & 0xFFu;
 }
 
 __device__ __forceinline__ void children_of(const uint64_t* bmp,
@@ -103,7 +100,12 @@ __device__ __forceinline__ uint32_t near_mask(int ox, int oy, int oz, int cr) {
 // One-time layout (per-level work and padded count segments) from the device
 // totals; written to global memory for the count / scan / write kernels.
 __global__ void k_lists_plan(const __grid_constant__ ListsParams p, ListsLayout* out) {
-  if (threadIdx.x == 0) lists_layout(p, *out);
+  if (threadIdx.x == 0) {
+    lists_layout(p, *out);
+    // every CSR starts at 0 (levels without receivers get no count-scan tile)
+    if (p.level >= 1) p.bm[0][0] = 0;
+    for (int l = 2; l <= p.level; ++l) p.bm[l][0] = 0;
+  }
 }
 
 __device__ __forceinline__ void load_layout(const ListsLayout* g, ListsLayout& s) {
@@ -170,44 +172,142 @@ __device__ __forceinline__ uint64_t popc_bytes(uint64_t x) {
   return (x + (x >> 4)) & 0x0F0F0F0F0F0F0F0Full;
 }
 
-// Count pass: per child receiver r of P, |E4_l(r)| (and |E2(r)| at l == L).
-// Lane = window slot; the near-children counts of all 8 child receivers come
-// from one SWAR byte-popcount and two warp reductions.
+// Count + CSR scan in one pass.  A tile is kCsParents consecutive receiver
+// parents P of one level (8 per warp); for each child receiver r of P it
+// counts |E4_l(r)| (and |E2(r)| at l == L) -- lane = window slot, the
+// near-children counts of all 8 children from one SWAR byte-popcount and two
+// warp reductions -- then the tile's rows (children in P order = ascending
+// receiver keys) are scanned in shared memory and offset by a decoupled
+// look-back over the level's tiles (tickets keep tiles in order).  Writes
+// the bookmark arrays and the per-level totals.
 __global__ void __launch_bounds__(kLThreads)
-    k_lists_count(const __grid_constant__ ListsParams p, const ListsLayout* __restrict__ glay) {
+    k_lists_cscan(const __grid_constant__ ListsParams p, const ListsLayout* __restrict__ glay,
+                  uint64_t* __restrict__ st4, uint64_t* __restrict__ st2,
+                  uint32_t* __restrict__ ticket, int64_t* __restrict__ seg_totals) {
   __shared__ ListsLayout lay;
+  __shared__ uint32_t s_rm[kCsParents], s_rf[kCsParents];
+  __shared__ uint16_t s_c4[kCsParents * 8], s_c2[kCsParents * 8];
+  __shared__ uint32_t s_w4[kLWarps], s_w2[kLWarps];
+  __shared__ int64_t s_tile, s_b4, s_b2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   load_layout(glay, lay);
+  if (tid == 0) s_tile = atomicAdd(ticket, 1u);
   __syncthreads();
   const int L = p.level;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t nwork = lay.work_off[L + 1];
-  const int64_t gstride = (int64_t)gridDim.x * kLWarps;
+  const int64_t tile = s_tile;
+  if (L == 0) {  // the root receiver sees the root source
+    if (tile == 0 && tid == 0) {
+      const int64_t kr = p.ktot[1], e2 = kr ? p.ktot[0] : 0;
+      p.bm[0][0] = 0;
+      if (kr) p.bm[0][1] = e2;
+      seg_totals[0] = e2;
+    }
+    return;
+  }
+  if (tile >= lay.tile_off[L + 1]) return;
+  int l = lay.lmin;
+  while (lay.tile_off[l + 1] <= tile) ++l;
+  const int64_t first_tile = lay.tile_off[l];
+  const int64_t np = lay.work_off[l + 1] - lay.work_off[l];
+  const int64_t j0 = (tile - first_tile) * kCsParents;
   const unsigned FULL = 0xffffffffu;
   const uint64_t nearw = lane < 27 ? kNear.w[lane] : 0ull;
-  for (int64_t gw = (int64_t)blockIdx.x * kLWarps + warp; gw < nwork; gw += gstride) {
-    int l = lay.lmin;
-    while (lay.work_off[l + 1] <= gw) ++l;
-    const int64_t j = gw - lay.work_off[l];
-    if (l == 0) {  // max level 0: the root receiver sees the root source
-      if (lane == 0) p.counts[lay.seg_off[0]] = (uint32_t)p.ktot[0];
-      continue;
+  constexpr int kPW = kCsParents / kLWarps;
+  for (int k = 0; k < kPW; ++k) {
+    const int pi = warp * kPW + k;
+    const int64_t j = j0 + pi;
+    uint32_t rm = 0, rfirst = 0, sm = 0;
+    if (j < np) {
+      const uint64_t P = __ldg(p.rkeys[l - 1] + j);
+      const uint64_t qk = window_key(P, l, lane);
+      if (qk != ~0ull) sm = children_mask(p.bmp + p.bmp_off[0][l], qk);
+      children_of(p.bmp + p.bmp_off[1][l], p.dir + p.bmp_off[1][l], P, rm, rfirst);
     }
-    const uint64_t P = __ldg(p.rkeys[l - 1] + j);
-    const uint64_t qk = window_key(P, l, lane);
-    uint32_t sm = 0, sfirst;
-    if (qk != ~0ull)
-      children_of(p.bmp + p.bmp_off[0][l], p.dir + p.bmp_off[0][l], qk, sm, sfirst);
-    uint32_t rm, rfirst;
-    children_of(p.bmp + p.bmp_off[1][l], p.dir + p.bmp_off[1][l], P, rm, rfirst);
     const uint64_t e2b = popc_bytes(((uint64_t)sm * 0x0101010101010101ull) & nearw);
     const uint32_t lo = __reduce_add_sync(FULL, (uint32_t)e2b);
     const uint32_t hi = __reduce_add_sync(FULL, (uint32_t)(e2b >> 32));
     const uint32_t all = __reduce_add_sync(FULL, (uint32_t)__popc(sm));
-    if (lane < 8 && ((rm >> lane) & 1u)) {
+    if (lane < 8) {
       const uint32_t e2 = ((lane < 4 ? lo >> (8 * lane) : hi >> (8 * (lane - 4)))) & 0xFFu;
-      const int64_t rrank = rfirst + __popc(rm & ((1u << lane) - 1u));
-      if (l >= 2) p.counts[lay.seg_off[l] + rrank] = all - e2;
-      if (l == L) p.counts[lay.seg_off[0] + rrank] = e2;
+      const bool has = (rm >> lane) & 1u;
+      s_c4[pi * 8 + lane] = (uint16_t)(has && l >= 2 ? all - e2 : 0u);
+      s_c2[pi * 8 + lane] = (uint16_t)(has ? e2 : 0u);
+    }
+    if (lane == 0) {
+      s_rm[pi] = rm;
+      s_rf[pi] = rfirst;
+    }
+  }
+  __syncthreads();
+  // exclusive scan over the tile's 64 x 8 child slots (empty slots count 0)
+  uint32_t a4 = s_c4[2 * tid], b4 = s_c4[2 * tid + 1];
+  uint32_t a2 = s_c2[2 * tid], b2 = s_c2[2 * tid + 1];
+  uint32_t t4, t2;
+  uint32_t x4 = warp_excl_scan(a4 + b4, t4);
+  uint32_t x2 = warp_excl_scan(a2 + b2, t2);
+  if (lane == 0) {
+    s_w4[warp] = t4;
+    s_w2[warp] = t2;
+  }
+  __syncthreads();
+  uint32_t tot4 = 0, tot2 = 0;
+#pragma unroll
+  for (int i = 0; i < kLWarps; ++i) {
+    x4 += i < warp ? s_w4[i] : 0u;
+    x2 += i < warp ? s_w2[i] : 0u;
+    tot4 += s_w4[i];
+    tot2 += s_w2[i];
+  }
+  const bool last = tile == lay.tile_off[l + 1] - 1;
+  if (tid == 0) {
+    uint64_t e4 = 0, e2 = 0;
+    if (l >= 2) {
+      uint64_t* st = st4 + tile;
+      if (tile == first_tile) {
+        st_state(st, kStInclusive | tot4);
+      } else {
+        st_state(st, kStAggregate | tot4);
+        e4 = lookback(st4, tile, first_tile, 1);
+        st_state(st, kStInclusive | (e4 + tot4));
+      }
+    }
+    if (l == L) {
+      uint64_t* st = st2 + tile;
+      if (tile == first_tile) {
+        st_state(st, kStInclusive | tot2);
+      } else {
+        st_state(st, kStAggregate | tot2);
+        e2 = lookback(st2, tile, first_tile, 1);
+        st_state(st, kStInclusive | (e2 + tot2));
+      }
+    }
+    s_b4 = (int64_t)e4;
+    s_b2 = (int64_t)e2;
+  }
+  __syncthreads();
+  const int64_t base4 = s_b4, base2 = s_b2;
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int slot = 2 * tid + e;
+    const int pi = slot >> 3, c = slot & 7;
+    const uint32_t rm = s_rm[pi];
+    if ((rm >> c) & 1u) {
+      const int64_t row = (int64_t)s_rf[pi] + __popc(rm & ((1u << c) - 1u));
+      if (l >= 2) p.bm[l][row] = base4 + x4;
+      if (l == L) p.bm[0][row] = base2 + x2;
+    }
+    x4 += e == 0 ? a4 : b4;
+    x2 += e == 0 ? a2 : b2;
+  }
+  if (last && tid == 0) {  // trailing bookmark = segment total
+    const int64_t kr = p.ktot[(L + 1) + l];
+    if (l >= 2) {
+      p.bm[l][kr] = base4 + tot4;
+      seg_totals[l] = base4 + tot4;
+    }
+    if (l == L) {
+      p.bm[0][kr] = base2 + tot2;
+      seg_totals[0] = base2 + tot2;
     }
   }
 }
@@ -351,74 +451,6 @@ __global__ void __launch_bounds__(kLThreads)
       const int64_t w4 = __ldg(p.bm[l] + rfirst);
       write_rows<true, false>(rm, meta, rank, r4 + w4, c4 + w4, nullptr);
     }
-  }
-}
-
-// Segmented exclusive scan of the padded count array into the i64 bookmark
-// arrays (one segment per list; segments start on tile boundaries and carry
-// a trailing zero so bookmark[K] = segment total).  Single pass, decoupled
-// look-back restarted at each segment's first tile.
-__global__ void __launch_bounds__(kScanThreads) k_lists_scan(const __grid_constant__ ListsParams p,
-                                                             const ListsLayout* __restrict__ glay,
-                                                             uint64_t* __restrict__ states,
-                                                             uint32_t* __restrict__ tile_counter,
-                                                             int64_t* __restrict__ seg_totals) {
-  __shared__ ListsLayout lay;
-  __shared__ int64_t s_tile, s_excl;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  load_layout(glay, lay);
-  if (tid == 0) s_tile = atomicAdd(tile_counter, 1u);
-  __syncthreads();
-  const int64_t tile = s_tile;
-  const int64_t ntiles = lay.seg_off[kMaxLevel + 1] / kScanTile;
-  if (tile >= ntiles) return;
-  int seg = 0;
-  while (lay.seg_off[seg + 1] / kScanTile <= tile) ++seg;
-  const int64_t first_tile = lay.seg_off[seg] / kScanTile;
-  const int64_t last_tile = lay.seg_off[seg + 1] / kScanTile - 1;
-  const int64_t e0 = (tile - first_tile) * kScanTile + tid * kScanItems;
-  const int64_t len = lay.seg_len[seg];
-  const uint32_t* cnt = p.counts + lay.seg_off[seg];
-  uint32_t v[kScanItems];
-  uint64_t c = 0;
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    const int64_t e = e0 + i;
-    v[i] = (e < len - 1) ? cnt[e] : 0u;  // the trailing entry is the total
-    c += v[i];
-  }
-  uint64_t wt;
-  const uint64_t x = warp_excl_scan<uint64_t>(c, wt);
-  __shared__ uint64_t s_w[kScanThreads / 32];
-  if (lane == 0) s_w[warp] = wt;
-  __syncthreads();
-  uint64_t off = 0, tot = 0;
-#pragma unroll
-  for (int i = 0; i < kScanThreads / 32; ++i) {
-    off += i < warp ? s_w[i] : 0ull;
-    tot += s_w[i];
-  }
-  if (tid == 0) {
-    uint64_t* st = states + tile;
-    uint64_t excl = 0;
-    if (tile == first_tile) {
-      st_state(st, kStInclusive | tot);
-    } else {
-      st_state(st, kStAggregate | tot);
-      excl = lookback(states, tile, first_tile, 1);
-      st_state(st, kStInclusive | (excl + tot));
-    }
-    s_excl = (int64_t)excl;
-    if (tile == last_tile) seg_totals[seg] = (int64_t)(excl + tot);
-  }
-  __syncthreads();
-  int64_t r = s_excl + (int64_t)(x + off);
-  int64_t* bm = p.bm[seg];
-#pragma unroll
-  for (int i = 0; i < kScanItems; ++i) {
-    const int64_t e = e0 + i;
-    if (e < len) bm[e] = r;
-    r += v[i];
   }
 }
 

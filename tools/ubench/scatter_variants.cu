@@ -88,11 +88,15 @@ __global__ void __launch_bounds__(kSThreads, 1)
     const int64_t i = lo + (int64_t)k * kSRows + tid;
     if (tid < stage_rows(k)) {
       const double w = i < n ? (q ? xyz[3 * kSRows + tid] : 0.0) : __longlong_as_double(i - n);
-      if (VAR == 5) rec[4 * (size_t)dst] = xyz[3 * tid];
+      if (VAR == 7) asm volatile("st.global.cs.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(rec + 4 * (size_t)dst), "d"(xyz[3 * tid]), "d"(xyz[3 * tid + 1]), "d"(xyz[3 * tid + 2]), "d"(w) : "memory");
+      else if (VAR == 8) asm volatile("st.global.L1::no_allocate.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(rec + 4 * (size_t)dst), "d"(xyz[3 * tid]), "d"(xyz[3 * tid + 1]), "d"(xyz[3 * tid + 2]), "d"(w) : "memory");
+      else if (VAR == 9) { uint64_t pol; asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+        asm volatile("st.global.L2::cache_hint.v4.f64 [%0], {%1, %2, %3, %4}, %5;" ::"l"(rec + 4 * (size_t)dst), "d"(xyz[3 * tid]), "d"(xyz[3 * tid + 1]), "d"(xyz[3 * tid + 2]), "d"(w), "l"(pol) : "memory"); }
+      else if (VAR == 5) rec[4 * (size_t)dst] = xyz[3 * tid];
       else if (VAR == 6) { reinterpret_cast<double2*>(rec)[2 * (size_t)dst] = make_double2(xyz[3 * tid], xyz[3 * tid + 1]);
                            reinterpret_cast<double2*>(rec)[2 * (size_t)dst + 1] = make_double2(xyz[3 * tid + 2], w); }
       else if (VAR != 2) st_v4f64(rec + 4 * (size_t)dst, xyz[3 * tid], xyz[3 * tid + 1], xyz[3 * tid + 2], w);
-      if (VAR != 2 && VAR != 3 && VAR != 5 && VAR != 6 && i < n) idx[dst] = (uint32_t)i;
+      if (VAR != 2 && VAR != 3 && VAR < 5 && i < n) idx[dst] = (uint32_t)i;
       if (VAR == 2 && dst == 0xFFFFFFFFu) idx[0] = 1;
     }
     mbar_arrive(empty + k % kSStages);
@@ -156,5 +160,8 @@ int main() {
   run("no idx store", k_var<true, 3>);
   run("8B store only (no idx)", k_var<true, 5>);
   run("2x16B store (no idx)", k_var<true, 6>);
+  run("st.cs (no idx)", k_var<true, 7>);
+  run("st.L1::no_allocate (no idx)", k_var<true, 8>);
+  run("st.L2 evict_last (no idx)", k_var<true, 9>);
   }
 }
