@@ -29,6 +29,7 @@ from .lists import (
     gather_adjacent_sources,
     propagate_to_parents,
 )
+from .scan import compact_flags, exclusive_scan
 from .pseudosort import (
     DEFAULT_HISTOGRAM_BUDGET,
     MAX_LEVEL,

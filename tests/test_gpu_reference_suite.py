@@ -18,6 +18,7 @@ REF = os.path.join(ROOT, "oracle", "_ref")
     "tests/test_lists.py",
     "tests/test_pseudosort.py",
     "tests/test_morton.py",
+    "tests/test_scan.py",
     "tests/test_acceptance.py::test_criterion_1_list_correctness",
     "tests/test_acceptance.py::test_criterion_2_single_count_coverage",
     "tests/test_acceptance.py::test_criterion_3_pseudo_sort_contract",

@@ -25,6 +25,12 @@ for _name in ("build_all", "sort_points", "histogram_and_sort_index", "reorder",
         if hasattr(_mod, _name):
             setattr(_mod, _name, _obj)
 
+import fmmkit.scan as _scan  # noqa: E402
+
+for _name in ("exclusive_scan", "compact_flags"):  # scan.py:25-81 -> device scan
+    setattr(fmmkit, _name, getattr(fb, _name))
+    setattr(_scan, _name, getattr(fb, _name))
+
 CALLS = {"build_all": 0}
 _orig_build_all = fb.build_all
 
