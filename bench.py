@@ -13,9 +13,13 @@ the public API with pinned host inputs and numpy outputs (H2D + D2H inside
 the timed region).  Inputs (0.94 GB at c2) exceed the 126 MB L2, so no flush
 is needed between steps.
 
-Multi-GPU (torchrun, N>1): every rank builds its own c2-sized workload
-(independent replicas, weak scaling, no collective on the data path); the
-Morton-partitioned single-problem build is paper_1301_1704_b200.distributed.
+Multi-GPU (torchrun, N>1): ONE problem partitioned by Morton-key ranges
+over NCCL (paper_1301_1704_b200.distributed: histogram all-reduce, all-to-all
+of the points, all-reduce of the occupancy bitmaps, owned lists per rank).
+Weak scaling: every rank contributes a c2-sized shard (N = M = 2^24 per GPU,
+uniform, seed 1 + rank), the global level is choose_max_level(N_global, 16)
+(the reference's cluster-size rule, pseudosort.py:22-29): L = 7, 7, 8, 8 at
+1, 2, 4, 8 GPUs.
 """
 
 from __future__ import annotations
@@ -340,10 +344,153 @@ def _numpy_bytes(st) -> int:
     return tot
 
 
+def run_partitioned(args):
+    """N > 1: the Morton-range partitioned build of one problem (NCCL)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1301_1704_b200 import distributed as D
+    from paper_1301_1704_b200 import roofline
+    from paper_1301_1704_b200.pseudosort import choose_max_level
+    from paper_1301_1704_b200.workloads import WORKLOADS, generate
+
+    ws, rank, local = dist_env()
+    local = local % torch.cuda.device_count()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    backend = os.environ.get("FMMB_DIST_BACKEND", "nccl")  # gloo: host-staged (testing)
+    if backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group(backend)
+    wl = WORKLOADS[args.workload]
+    n_per = wl.n
+    n_glob = n_per * ws
+    L = choose_max_level(n_glob, 16)
+    src_np, q_np, recv_np = generate(n_per, n_per, wl.dist, wl.seed + rank)
+    src = torch.from_numpy(src_np).to(dev)
+    q = torch.from_numpy(q_np).to(dev)
+    recv = torch.from_numpy(recv_np).to(dev)
+    comm = D.TorchComm()
+    ops = D.DeviceOps()
+
+    def step():
+        return D.build_all_distributed([(src, q, recv)], L, comm, ops=ops)[0]
+
+    sh = None
+    for _ in range(max(args.warmup, 3)):
+        sh = None
+        sh = step()
+    pts = int(sh.sorted_src.points.shape[0] + sh.sorted_recv.points.shape[0])
+    sent = int(sh.exchanged["sent_points"])
+    lists_bytes = 8 * int(sh.neighbor_table.neighbor_list.shape[0]) + sum(
+        10 * int(v.shape[0]) for v in sh.stencils.ranks.values())
+    sh = None
+    torch.cuda.synchronize()
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    dist.barrier()
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream(dev)
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ops.launches = 0
+    ev0.record(stream)
+    for _ in range(args.steps):
+        sh = step()
+        sh = None
+    ev1.record(stream)
+    launches = ops.launches
+    torch.cuda.synchronize()
+    dist.barrier()
+    clk = clocks.stop()
+    t = torch.tensor([ev0.elapsed_time(ev1) * 1e-3], device=dev, dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    elapsed = float(t.item())
+    agg = torch.tensor([pts, sent, lists_bytes], device=dev, dtype=torch.int64)
+    dist.all_reduce(agg)
+    pts_all, sent_all, lists_all = (int(x) for x in agg.tolist())
+    ms_step = elapsed / args.steps * 1e3
+    value = 2 * n_glob * args.steps / elapsed
+    # per-GPU algorithmic bytes: inputs + sorted outputs (SURVEY 8(d), 80/64 B per
+    # src/recv point) + the lists this rank owns, against its share of the step
+    per_gpu_bytes = (80 + 64) / 2 * pts_all / ws + lists_all / ws
+    achieved = per_gpu_bytes / (elapsed / args.steps) / 1e9
+    peak, peak_src = roofline.measured_hbm_gbs(ROOT)
+    e2e = None
+    if not args.no_e2e:
+        h_src = torch.from_numpy(src_np).pin_memory()
+        h_q = torch.from_numpy(q_np).pin_memory()
+        h_recv = torch.from_numpy(recv_np).pin_memory()
+        times = []
+        d2h = 0
+        for _ in range(max(1, args.e2e_steps)):
+            torch.cuda.synchronize()
+            dist.barrier()
+            t0 = time.perf_counter()
+            shard = [(h_src.to(dev, non_blocking=True), h_q.to(dev, non_blocking=True),
+                      h_recv.to(dev, non_blocking=True))]
+            out = D.build_all_distributed(shard, L, comm)[0].to_numpy()
+            dt = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            times.append(float(dt.item()))
+            d2h = _numpy_bytes_shard(out)
+            out = None
+        h2d = (h_src.numel() + h_q.numel() + h_recv.numel()) * 8
+        e2e = {"value": 2 * n_glob / statistics.median(times), "unit": UNIT,
+               "h2d_bytes_per_step": int(h2d * ws), "d2h_bytes_per_step": int(d2h * ws),
+               "ms_per_step": statistics.median(times) * 1e3}
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64/u64 (integer keys, f64 points)",
+            "data": "synthetic (fmmkit.cli.generate Philox streams, seed 1 + rank)",
+            "config": {
+                "workload": f"{wl.name} shard per GPU: N=M={n_per} {wl.dist} per rank, "
+                            f"global N=M={n_glob}, max_level={L} (cluster size 16)",
+                "global_batch_particles": 2 * n_glob,
+                "parallelism": f"{ws}-way Morton-range partition ({backend} all-reduce + all-to-all)",
+                "l2": "inputs larger than the 126 MB L2; no flush",
+            },
+            "roofline": {
+                "bound": "hbm", "kernel": "whole partitioned step per GPU",
+                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "peak_source": peak_src, "traffic": None,
+            },
+            "exchange": {"points_sent": sent_all,
+                         "bytes_sent": sent_all * 40,
+                         "nvlink_gbs_per_gpu_at_step": sent_all * 40 / ws / (elapsed / args.steps) / 1e9},
+            "clocks": clk,
+            "e2e": e2e,
+            "cpu_baseline": None,
+            "gpu_launches": int(launches),
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
+def _numpy_bytes_shard(sh) -> int:
+    tot = 0
+    for ps in (sh.sorted_src, sh.sorted_recv):
+        for f in ("points", "charges", "permutation", "bookmarks", "non_empty_index", "boxes"):
+            v = getattr(ps, f)
+            if v is not None:
+                tot += v.nbytes
+    tot += sh.neighbor_table.neighbor_bookmark.nbytes + sh.neighbor_table.neighbor_list.nbytes
+    for l in sh.stencils.ranks:
+        tot += (sh.stencils.bookmark[l].nbytes + sh.stencils.ranks[l].nbytes
+                + sh.stencils.codes[l].nbytes)
+    return tot
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference_arm(args)
+    elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        run_partitioned(args)
     else:
         run_ours(args)
 

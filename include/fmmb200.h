@@ -208,6 +208,52 @@ FMMB_API fmmb_status fmmb_sort_points(fmmb_handle_t h, const double* points,
                              fmmb_alloc_fn alloc, void* ctx,
                              fmmb_point_set* out, void* stream);
 
+/* ------------------------------------------- multi-GPU (Morton partition) */
+/* The build of one problem across P GPUs (PAPER.md:923-948,
+ * partition.py:22-61 for the contiguous-range ownership).  The host drives
+ * the collectives between these calls (paper_1301_1704_b200/distributed.py):
+ *   fmmb_part_histogram -> all-reduce -> cut bins into P ranges ->
+ *   fmmb_part_pack -> all-to-all -> fmmb_dist_sort -> all-reduce (SUM = OR)
+ *   of the level-L bitmaps -> fmmb_dist_lists.
+ * The concatenation over ranks of every output equals fmmb_build_all on the
+ * whole problem. */
+
+/* Histogram of the top `pbits` (<= 14, <= 3L) level-L Morton-key bits over
+ * [src | recv] into hist[2^pbits] (u32, device). */
+FMMB_API fmmb_status fmmb_part_histogram(fmmb_handle_t h, const double* src, int64_t n,
+                                const double* recv, int64_t m, int level, int pbits,
+                                uint32_t* hist, void* stream);
+
+/* Stable partition of [src | recv] by destination rank bin_rank[bin] into
+ * send buffers grouped by destination (input order kept inside a group):
+ * sxyz (n,3), sq (n) or NULL, sgid (n) = gbase_src + local index, rxyz (m,3),
+ * rgid (m).  counts (HOST, 2*nranks): points per destination, src then recv. */
+FMMB_API fmmb_status fmmb_part_pack(fmmb_handle_t h, const double* src, const double* q,
+                           int64_t n, const double* recv, int64_t m, int level, int pbits,
+                           const uint32_t* bin_rank, int nranks, int64_t gbase_src,
+                           int64_t gbase_recv, double* sxyz, double* sq, int64_t* sgid,
+                           double* rxyz, int64_t* rgid, int64_t* counts, void* stream);
+
+/* Sort phase of one rank's owned points (global indices gid_*): sorted
+ * point sets with rank-local bookmarks / non-empty keys and permutations in
+ * GLOBAL indices, plus the level-L occupancy bitmaps (bmp: 2 * max(1,8^L/64)
+ * u64 words, src then recv) for the all-reduce. */
+FMMB_API fmmb_status fmmb_dist_sort(fmmb_handle_t h, const double* src, const double* q,
+                           int64_t n, const int64_t* gid_src, const double* recv, int64_t m,
+                           const int64_t* gid_recv, int level, fmmb_alloc_fn alloc, void* ctx,
+                           fmmb_point_set* src_out, fmmb_point_set* recv_out, uint64_t* bmp,
+                           void* stream);
+
+/* Lists of one rank from the GLOBAL level-L bitmaps (gbmp, layout as above):
+ * receiver rows owned by the key window [key_lo, key_hi) at every level (a
+ * box is owned when its first level-L key is), E2/E4 entries as global
+ * source ranks, CSR bookmarks starting at 0 (the host adds the offsets of
+ * the preceding ranks), owned windows of the level directory (levels 2..L-1).
+ * out->recv.k = owned level-L rows. */
+FMMB_API fmmb_status fmmb_dist_lists(fmmb_handle_t h, const uint64_t* gbmp, int level,
+                            uint64_t key_lo, uint64_t key_hi, fmmb_alloc_fn alloc, void* ctx,
+                            fmmb_structures* out, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -76,6 +76,15 @@ SIGNATURES = [
      [_p, _p, _p, _i64, _p, _i64, C.c_int, ALLOC_FN, _p, C.POINTER(StructuresC), _p, _p]),
     ("fmmb_sort_points", C.c_int,
      [_p, _p, _p, _i64, C.c_int, ALLOC_FN, _p, C.POINTER(PointSetC), _p]),
+    ("fmmb_part_histogram", C.c_int, [_p, _p, _i64, _p, _i64, C.c_int, C.c_int, _p, _p]),
+    ("fmmb_part_pack", C.c_int,
+     [_p, _p, _p, _i64, _p, _i64, C.c_int, C.c_int, _p, C.c_int, _i64, _i64, _p, _p, _p, _p,
+      _p, C.POINTER(_i64), _p]),
+    ("fmmb_dist_sort", C.c_int,
+     [_p, _p, _p, _i64, _p, _p, _i64, _p, C.c_int, ALLOC_FN, _p, C.POINTER(PointSetC),
+      C.POINTER(PointSetC), _p, _p]),
+    ("fmmb_dist_lists", C.c_int,
+     [_p, _p, C.c_int, C.c_uint64, C.c_uint64, ALLOC_FN, _p, C.POINTER(StructuresC), _p]),
 ]
 
 _lib = None

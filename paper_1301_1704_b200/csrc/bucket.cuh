@@ -468,7 +468,15 @@ struct LocalOut {
   int64_t* bm;
   unsigned long long* bmp[2];  // level-L occupancy bitmaps (may be null)
   int64_t* kinfo;
+  const int64_t* gid[2];  // multi-GPU: global index of each local src / recv point (or null)
 };
+
+// permutation entry: local input index -> global index under the multi-GPU
+// partition (identity for a single-GPU build)
+__device__ __forceinline__ int64_t perm_of(const LocalOut& o, int set, int64_t local) {
+  const int64_t* g = set ? o.gid[1] : o.gid[0];
+  return g ? __ldg(g + local) : local;
+}
 
 // Ranking inside a bucket: with HEADS and <= 2^kLcSmallBits boxes per bucket,
 // per-box counts (shared atomics), unstable placement into box segments and a
@@ -654,9 +662,9 @@ __global__ void __launch_bounds__(kLcThreads)
       po[2] = r[2];
       if (set == 0) {
         if (o.q) o.q[p] = r[3];
-        o.perm[p] = (int64_t)s_idx[j];
+        o.perm[p] = perm_of(o, 0, (int64_t)s_idx[j]);
       } else {
-        o.perm[p] = __double_as_longlong(r[3]);
+        o.perm[p] = perm_of(o, 1, __double_as_longlong(r[3]));
       }
       o.boxes[p] = prefix | (uint64_t)k0[j];
     }
@@ -735,9 +743,9 @@ __global__ void __launch_bounds__(kLcThreads)
       po[2] = r[2];
       if (set == 0) {
         if (o.q) o.q[p] = r[3];
-        o.perm[p] = (int64_t)s_idx[pl];
+        o.perm[p] = perm_of(o, 0, (int64_t)s_idx[pl]);
       } else {
-        o.perm[p] = __double_as_longlong(r[3]);
+        o.perm[p] = perm_of(o, 1, __double_as_longlong(r[3]));
       }
       o.boxes[p] = mk;
       const int64_t incl = hbase + woff + __popc(hb & (lt | (1u << lane)));

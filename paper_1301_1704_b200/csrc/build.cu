@@ -21,6 +21,7 @@
 #include "internal.h"
 #include "common.cuh"
 #include "bucket.cuh"
+#include "dist.cuh"
 #include "finalize.cuh"
 #include "lists.cuh"
 #include "sort.cuh"
@@ -85,6 +86,8 @@ extern "C" fmmb_status fmmb_create(int device, fmmb_handle_t* out) {
                        (int)scatter_smem_bytes());
   cudaFuncSetAttribute(k_bkt_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)scatter_smem_bytes());
+  cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)(sizeof(uint32_t) << kPartMaxBits));
 #define FMMB_LCATTR(CK, NW, HD)                                                        \
   cudaFuncSetAttribute(k_bkt_local<CK, NW, HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
                        (int)lc_smem_bytes<CK>())
@@ -305,17 +308,25 @@ fmmb_status sort_onesweep(fmmb_handle_t h, const double* src, const double* q, i
   }
   k_gather<KeyT><<<(unsigned)gather_tiles, kGThreads, gather_smem_bytes(), s>>>(
       ka, va, n, m, L, src, q, recv, o.pts, o.q, o.perm, o.boxes, o.ne, o.bm, o.bmp[0], o.bmp[1],
-      (uint64_t*)(w + o_gst), tc + 8, o.kinfo);
+      (uint64_t*)(w + o_gst), tc + 8, o.kinfo, o.gid[0], o.gid[1]);
   ++launches;
   cudaFreeAsync(w, s);
   return FMMB_OK;
 }
 
+// Multi-GPU sort phase extras: global indices of the local points and the
+// caller's level-L occupancy bitmaps (src words then recv words).
+struct DistSortArgs {
+  const int64_t* gid_src;
+  const int64_t* gid_recv;
+  uint64_t* bmp;
+};
+
 template <typename KeyT>
 fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int64_t n,
                        const double* recv, int64_t m, int L, fmmb_alloc_fn alloc,
                        void* ctx, fmmb_structures* out, cudaEvent_t* ev,
-                       cudaStream_t s, bool lists) {
+                       cudaStream_t s, bool lists, const DistSortArgs* dsa = nullptr) {
   const int64_t tot = n + m;
   const int stride = L + 1;
 
@@ -400,6 +411,14 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
   lo.bmp[0] = lists ? (unsigned long long*)(bmp + rp.word_off[L]) : nullptr;
   lo.bmp[1] = lists ? (unsigned long long*)(bmp + rp.word_off[stride + L]) : nullptr;
   lo.kinfo = dplan->kinfo;
+  if (dsa) {
+    lo.gid[0] = dsa->gid_src;
+    lo.gid[1] = dsa->gid_recv;
+    if (dsa->bmp) {
+      lo.bmp[0] = (unsigned long long*)dsa->bmp;
+      lo.bmp[1] = (unsigned long long*)(dsa->bmp + level_words(L));
+    }
+  }
 
   int64_t launches = 0;
   bool fast = h->sort_path != 2 && tot > 0;
@@ -410,6 +429,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     if (ev) cudaEventRecord(ev[0], s);
     cudaMemsetAsync(ws, 0, zero_bytes, s);
     if (tot == 0) cudaMemsetAsync(bm_out, 0, 2 * sizeof(int64_t), s);
+    if (dsa && dsa->bmp) cudaMemsetAsync(dsa->bmp, 0, 2 * level_words(L) * sizeof(uint64_t), s);
 
     // ---- K1-K4: sort both sets into the reference layout
     BucketRun brun;
@@ -490,6 +510,8 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     nwork_cap = 0;
     if (lists) {
       lp.level = L;
+      lp.key_lo = 0;
+      lp.key_hi = 1ull << (3 * L);
       lp.ktot = dplan->ktot;
       lp.bmp = bmp;
       lp.dir = dir;
@@ -535,7 +557,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
                      "(coordinates must lie in the unit cube)", L);
   }
   const int64_t ks = lists ? hp->ktot[L] : (n > 0 ? hp->kinfo[0] : 0);
-  const int64_t kr = lists ? hp->ktot[stride + L] : 0;
+  const int64_t kr = lists ? hp->ktot[stride + L] : (m > 0 ? hp->kinfo[1] - ks : 0);
   if (lists && tot > 0 && (hp->kinfo[0] != ks || (m > 0 && hp->kinfo[1] != ks + kr))) {
     cudaFreeAsync(ws, s);
     return fmmb_fail(h, FMMB_ERR_CUDA, "internal: box counts disagree (%lld/%lld vs %lld/%lld)",
@@ -678,3 +700,4 @@ extern "C" fmmb_status fmmb_sort_points(fmmb_handle_t h, const double* points,
 }
 
 #include "plugin.cuh"
+#include "dist_api.cuh"

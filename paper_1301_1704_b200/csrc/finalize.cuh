@@ -40,7 +40,8 @@ __global__ void __launch_bounds__(kGThreads)
              unsigned long long* __restrict__ bmp_src,
              unsigned long long* __restrict__ bmp_recv,
              uint64_t* __restrict__ states, uint32_t* __restrict__ tile_counter,
-             int64_t* __restrict__ kinfo) {
+             int64_t* __restrict__ kinfo, const int64_t* __restrict__ gid_src,
+             const int64_t* __restrict__ gid_recv) {
   extern __shared__ __align__(16) unsigned char smem[];
   double* s_pts = reinterpret_cast<double*>(smem);
   uint32_t* s_cnt = reinterpret_cast<uint32_t*>(s_pts + kGTile * 3);  // [items][warps]
@@ -105,7 +106,7 @@ __global__ void __launch_bounds__(kGThreads)
     s_pts[3 * r + 0] = __ldg(row);
     s_pts[3 * r + 1] = __ldg(row + 1);
     s_pts[3 * r + 2] = __ldg(row + 2);
-    perm_out[p] = orig;
+    perm_out[p] = set ? (gid_recv ? gid_recv[orig] : orig) : (gid_src ? gid_src[orig] : orig);
     boxes_out[p] = mk;
     if (!set && q) q_out[p] = __ldg(q + orig);
     // inclusive count of heads up to p = (combined rank of p's box) + 1

@@ -35,6 +35,10 @@ struct ListsParams {
   int64_t* bm[kMaxLevel + 1];            // bookmark arrays per segment
   int64_t* ranks_out[kMaxLevel + 1];     // write pass: [0]=E2 list, [l]=E4 ranks
   int16_t* codes_out[kMaxLevel + 1];     // [l]=E4 codes
+  // finest-level key window [key_lo, key_hi) owned by this build (the whole
+  // grid for a single-GPU build; a Morton range under the multi-GPU
+  // partition).  A level-l box is owned when its first finest-level key is.
+  uint64_t key_lo, key_hi;
 };
 
 // Per-level work and segment layout, recomputed per block from the device
@@ -43,23 +47,54 @@ struct ListsLayout {
   int lmin;                     // first level with work
   int64_t work_off[kMaxLevel + 2];  // prefix of receiver-parent counts
   int64_t tile_off[kMaxLevel + 2];  // prefix of count-scan tiles per level
+  int64_t r_lo[kMaxLevel + 1];      // owned receiver rows at level l: ranks [r_lo, r_hi)
+  int64_t r_hi[kMaxLevel + 1];
+  int64_t p_lo[kMaxLevel + 1];      // first receiver parent (rank at level l-1) with an owned row
+  int64_t rs_lo[kMaxLevel + 1];     // owned source boxes at level l: ranks [rs_lo, rs_hi)
+  int64_t rs_hi[kMaxLevel + 1];
 };
 
 constexpr int kCsParents = 64;  // receiver parents per count-scan tile (8 per warp)
 
 __device__ __forceinline__ int lists_lmin(int L) { return L >= 2 ? 2 : L; }
 
+// rank of `key` among the set bits of (set, level l): boxes with smaller keys
+__device__ inline int64_t level_rank(const ListsParams& p, int set, int l, uint64_t key) {
+  const int L = p.level;
+  if (key >= (1ull << (3 * l))) return p.ktot[set * (L + 1) + l];
+  const uint64_t* bmp = p.bmp + p.bmp_off[set][l];
+  const uint32_t* dir = p.dir + p.bmp_off[set][l];
+  const uint64_t w = key >> 6;
+  return (int64_t)dir[w] + __popcll(bmp[w] & ((1ull << (key & 63)) - 1ull));
+}
+
 __device__ inline void lists_layout(const ListsParams& p, ListsLayout& lay) {
   const int L = p.level;
-  const int stride = L + 1;
   lay.lmin = lists_lmin(L);
   int64_t w = 0, t = 0;
   for (int l = 0; l <= kMaxLevel + 1; ++l) lay.work_off[l] = lay.tile_off[l] = 0;
+  for (int l = 0; l <= kMaxLevel; ++l)
+    lay.r_lo[l] = lay.r_hi[l] = lay.p_lo[l] = lay.rs_lo[l] = lay.rs_hi[l] = 0;
   for (int l = 0; l <= L; ++l) {
     lay.work_off[l] = w;
     lay.tile_off[l] = t;
+    const int sh = 3 * (L - l);
+    const uint64_t b_lo = (p.key_lo + (1ull << sh) - 1ull) >> sh;  // ceil
+    const uint64_t b_hi = (p.key_hi + (1ull << sh) - 1ull) >> sh;
+    lay.r_lo[l] = level_rank(p, 1, l, b_lo);
+    lay.r_hi[l] = level_rank(p, 1, l, b_hi);
+    lay.rs_lo[l] = level_rank(p, 0, l, b_lo);
+    lay.rs_hi[l] = level_rank(p, 0, l, b_hi);
     if (l >= lay.lmin) {
-      const int64_t np = (l == 0) ? p.ktot[stride + 0] : p.ktot[stride + l - 1];
+      int64_t np;
+      if (l == 0) {
+        np = p.ktot[(L + 1) + 0];
+      } else if (b_hi > b_lo) {
+        lay.p_lo[l] = level_rank(p, 1, l - 1, b_lo >> 3);
+        np = level_rank(p, 1, l - 1, ((b_hi - 1) >> 3) + 1) - lay.p_lo[l];
+      } else {
+        np = 0;
+      }
       w += np;
       t += (np + kCsParents - 1) / kCsParents;
     }
@@ -103,8 +138,9 @@ __global__ void k_lists_plan(const __grid_constant__ ListsParams p, ListsLayout*
   if (threadIdx.x == 0) {
     lists_layout(p, *out);
     // every CSR starts at 0 (levels without receivers get no count-scan tile)
-    if (p.level >= 1) p.bm[0][0] = 0;
-    for (int l = 2; l <= p.level; ++l) p.bm[l][0] = 0;
+    if (p.level >= 1 && p.bm[0]) p.bm[0][0] = 0;
+    for (int l = 2; l <= p.level; ++l)
+      if (p.bm[l]) p.bm[l][0] = 0;
   }
 }
 
@@ -218,7 +254,7 @@ __global__ void __launch_bounds__(kLThreads)
     const int64_t j = j0 + pi;
     uint32_t rm = 0, rfirst = 0, sm = 0;
     if (j < np) {
-      const uint64_t P = __ldg(p.rkeys[l - 1] + j);
+      const uint64_t P = __ldg(p.rkeys[l - 1] + lay.p_lo[l] + j);
       const uint64_t qk = window_key(P, l, lane);
       if (qk != ~0ull) sm = children_mask(p.bmp + p.bmp_off[0][l], qk);
       children_of(p.bmp + p.bmp_off[1][l], p.dir + p.bmp_off[1][l], P, rm, rfirst);
@@ -229,7 +265,8 @@ __global__ void __launch_bounds__(kLThreads)
     const uint32_t all = __reduce_add_sync(FULL, (uint32_t)__popc(sm));
     if (lane < 8) {
       const uint32_t e2 = ((lane < 4 ? lo >> (8 * lane) : hi >> (8 * (lane - 4)))) & 0xFFu;
-      const bool has = (rm >> lane) & 1u;
+      const int64_t row = (int64_t)rfirst + __popc(rm & ((1u << lane) - 1u));
+      const bool has = ((rm >> lane) & 1u) && row >= lay.r_lo[l] && row < lay.r_hi[l];
       s_c4[pi * 8 + lane] = (uint16_t)(has && l >= 2 ? all - e2 : 0u);
       s_c2[pi * 8 + lane] = (uint16_t)(has ? e2 : 0u);
     }
@@ -291,8 +328,8 @@ __global__ void __launch_bounds__(kLThreads)
     const int slot = 2 * tid + e;
     const int pi = slot >> 3, c = slot & 7;
     const uint32_t rm = s_rm[pi];
-    if ((rm >> c) & 1u) {
-      const int64_t row = (int64_t)s_rf[pi] + __popc(rm & ((1u << c) - 1u));
+    const int64_t row = (int64_t)s_rf[pi] + __popc(rm & ((1u << c) - 1u)) - lay.r_lo[l];
+    if (((rm >> c) & 1u) && row >= 0 && row < lay.r_hi[l] - lay.r_lo[l]) {
       if (l >= 2) p.bm[l][row] = base4 + x4;
       if (l == L) p.bm[0][row] = base2 + x2;
     }
@@ -300,7 +337,7 @@ __global__ void __launch_bounds__(kLThreads)
     x2 += e == 0 ? a2 : b2;
   }
   if (last && tid == 0) {  // trailing bookmark = segment total
-    const int64_t kr = p.ktot[(L + 1) + l];
+    const int64_t kr = lay.r_hi[l] - lay.r_lo[l];
     if (l >= 2) {
       p.bm[l][kr] = base4 + tot4;
       seg_totals[l] = base4 + tot4;
@@ -395,7 +432,7 @@ __global__ void __launch_bounds__(kLThreads)
       if (lane == 0 && p.ktot[0]) p.ranks_out[0][p.bm[0][0]] = 0;
       continue;
     }
-    const uint64_t P = __ldg(p.rkeys[l - 1] + j);
+    const uint64_t P = __ldg(p.rkeys[l - 1] + lay.p_lo[l] + j);
     uint64_t qk = window_key(P, l, lane);
     int o = lane;
 #pragma unroll
@@ -439,6 +476,24 @@ __global__ void __launch_bounds__(kLThreads)
     int64_t* r4 = p.ranks_out[l];
     int16_t* c4 = p.codes_out[l];
     int64_t* r2 = p.ranks_out[0];
+    // owned children (a contiguous run of ranks) and the first one's CSR row
+    uint32_t own = 0;
+    int64_t r0 = -1;
+    {
+      int64_t r = rfirst;
+#pragma unroll
+      for (int c = 0; c < 8; ++c)
+        if ((rm >> c) & 1u) {
+          if (r >= lay.r_lo[l] && r < lay.r_hi[l]) {
+            own |= 1u << c;
+            if (r0 < 0) r0 = r - lay.r_lo[l];
+          }
+          ++r;
+        }
+    }
+    rm = own;
+    if (!rm) continue;
+    rfirst = (uint32_t)r0;
     if (l == L) {
       const int64_t w2 = __ldg(p.bm[0] + rfirst);
       if (l >= 2) {

@@ -1,0 +1,455 @@
+"""Multi-GPU build of ONE problem by contiguous Morton-key ranges.
+
+The paper's scheme (reference ownership by key range:
+pkg/src/fmmkit/partition.py:22-61, distributed build: exchange.py:183-272),
+one process per GPU, the collectives through `torch.distributed` (NCCL over
+NVLink on the B200 box):
+
+ 1. every rank holds an index-contiguous shard of the sources and receivers;
+ 2. histogram of the top `pbits` level-L key bits (device), all-reduce, and a
+    deterministic cut of the bins into P contiguous ranges balancing src+recv
+    points -- a box never straddles two ranks;
+ 3. stable pack by destination (device) and an all-to-all of (xyz, q, global
+    index); receive order is (source rank, index) = global index order, so
+    the local stable sort reproduces the global order;
+ 4. local sort phase (`fmmb_dist_sort`): sorted points, permutation in global
+    indices, rank-local bookmarks, level-L occupancy bitmaps;
+ 5. all-reduce (SUM = OR: the ranks' bits are disjoint) of the bitmaps;
+ 6. lists of the receiver rows the rank owns (a level-l box is owned by the
+    rank whose key range holds its first level-L key), with global source
+    ranks (`fmmb_dist_lists`);
+ 7. an all-gather of the shard sizes turns rank-local CSR / bookmark offsets
+    into global ones.
+
+Every rank ends up with a contiguous shard of every `FmmStructures` array;
+`concat_shards` of the shards in rank order is bit-identical to the
+single-GPU `build_all` of the whole problem.
+
+The collectives go through a small `Comm` interface: `TorchComm` (one rank
+per process, torch.distributed -- NCCL, or gloo with host staging) and
+`SimComm` (all ranks driven by one process; used to test and measure the
+partitioned path on a single GPU).  The per-rank device steps go through an
+`ops` object (`DeviceOps`, the libfmmb200 kernels; there is no CPU fallback).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DomainError
+from .lists import FmmStructures, LevelDirectory, NeighborTable, TranslationStencils
+from .pseudosort import SortedPointSet, _point_set_from_c, check_level
+
+__all__ = [
+    "Comm", "TorchComm", "SimComm", "DeviceOps", "DistShard", "build_all_distributed",
+    "cut_bins", "concat_shards", "partition_bits",
+]
+
+
+# ------------------------------------------------------------------ comms
+class Comm:
+    """Collectives over `size` ranks; `ranks` are the ranks this process
+    drives (one for TorchComm, all of them for SimComm).  Every method takes
+    one entry per driven rank, in `ranks` order, and returns the same."""
+
+    size: int
+    ranks: list
+
+    def allreduce_sum(self, xs: list) -> list:
+        raise NotImplementedError
+
+    def all_to_all(self, chunks: list) -> list:
+        """chunks[i][d] = tensor from driven rank i to rank d; returns
+        out[i][s] = tensor rank ranks[i] received from rank s."""
+        raise NotImplementedError
+
+    def all_gather(self, xs: list) -> list:
+        """out[i] = [x of rank 0, ..., x of rank size-1] (same shapes)."""
+        raise NotImplementedError
+
+
+class SimComm(Comm):
+    """All `size` ranks in this process (their tensors may share a device)."""
+
+    def __init__(self, size: int):
+        self.size = size
+        self.ranks = list(range(size))
+
+    def allreduce_sum(self, xs):
+        tot = xs[0].clone()
+        for x in xs[1:]:
+            tot += x
+        return [tot.clone() for _ in xs]
+
+    def all_to_all(self, chunks):
+        return [[chunks[s][d] for s in range(self.size)] for d in range(self.size)]
+
+    def all_gather(self, xs):
+        return [list(xs) for _ in xs]
+
+
+class TorchComm(Comm):
+    """One rank per process over a torch.distributed process group (NCCL for
+    CUDA tensors; gloo stages CUDA tensors through the host)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+
+        self.dist = dist
+        self.group = group
+        self.size = dist.get_world_size(group)
+        self.ranks = [dist.get_rank(group)]
+        self.stage = dist.get_backend(group) == "gloo"
+
+    def _to(self, x):
+        return x.cpu() if self.stage else x
+
+    def allreduce_sum(self, xs):
+        (x,) = xs
+        y = self._to(x).clone()
+        self.dist.all_reduce(y, group=self.group)
+        return [y.to(x.device)]
+
+    def all_to_all(self, chunks):
+        (row,) = chunks
+        dev = row[0].device
+        dtype = row[0].dtype
+        tail = tuple(row[0].shape[1:])
+        width = int(np.prod(tail)) if tail else 1
+        sizes = torch.tensor([int(c.shape[0]) for c in row], dtype=torch.int64)
+        if not self.stage:
+            sizes = sizes.to(dev)
+        rsizes = torch.empty_like(sizes)
+        self.dist.all_to_all_single(rsizes, sizes, group=self.group)
+        rs = rsizes.cpu().tolist()
+        send = self._to(torch.cat([c.reshape(-1) for c in row]))
+        recv = torch.empty(sum(rs) * width, dtype=dtype, device=send.device)
+        self.dist.all_to_all_single(recv, send, [r * width for r in rs],
+                                    [int(c.shape[0]) * width for c in row], group=self.group)
+        recv = recv.to(dev)
+        out, at = [], 0
+        for r in rs:
+            out.append(recv[at: at + r * width].reshape((r,) + tail))
+            at += r * width
+        return [out]
+
+    def all_gather(self, xs):
+        (x,) = xs
+        outs = [torch.empty_like(self._to(x)) for _ in range(self.size)]
+        self.dist.all_gather(outs, self._to(x).contiguous(), group=self.group)
+        return [[o.to(x.device) for o in outs]]
+
+
+# ------------------------------------------------------------- device ops
+@dataclass
+class DistLists:
+    neighbor_bookmark: torch.Tensor
+    neighbor_list: torch.Tensor
+    dir_src: dict
+    dir_recv: dict
+    st_bookmark: dict
+    st_ranks: dict
+    st_codes: dict
+
+
+class DeviceOps:
+    """The per-rank device steps, on libfmmb200 (include/fmmb200.h).
+    `launches` counts the library's kernel launches."""
+
+    def __init__(self):
+        self.launches = 0
+
+    def _count(self, h):
+        self.launches += int(_lib.load().fmmb_last_launch_count(h))
+
+    def part_histogram(self, src, recv, level, pbits):
+        dev = _lib.device_of(src.device)
+        h = _lib.handle(dev)
+        hist = torch.empty(1 << pbits, dtype=torch.int32, device=dev)  # u32 counts < 2^31
+        n, m = int(src.shape[0]), int(recv.shape[0])
+        st = _lib.load().fmmb_part_histogram(
+            h, src.data_ptr() if n else None, n, recv.data_ptr() if m else None, m, level,
+            pbits, hist.data_ptr(), _lib.stream_of(dev))
+        _lib.check(st, h)
+        self._count(h)
+        return hist.to(torch.int64)
+
+    def part_pack(self, src, q, recv, level, pbits, bin_rank, nranks, gbase_src, gbase_recv):
+        dev = _lib.device_of(src.device)
+        h = _lib.handle(dev)
+        n, m = int(src.shape[0]), int(recv.shape[0])
+        sxyz = torch.empty((n, 3), dtype=torch.float64, device=dev)
+        sq = torch.empty(n, dtype=torch.float64, device=dev) if q is not None else None
+        sgid = torch.empty(n, dtype=torch.int64, device=dev)
+        rxyz = torch.empty((m, 3), dtype=torch.float64, device=dev)
+        rgid = torch.empty(m, dtype=torch.int64, device=dev)
+        counts = (C.c_int64 * (2 * nranks))()
+        br = bin_rank.to(device=dev, dtype=torch.int32).contiguous()
+        p = lambda t: t.data_ptr() if (t is not None and t.numel()) else None  # noqa: E731
+        st = _lib.load().fmmb_part_pack(
+            h, p(src), p(q), n, p(recv), m, level, pbits, br.data_ptr(), nranks, gbase_src,
+            gbase_recv, p(sxyz), p(sq), p(sgid), p(rxyz), p(rgid), counts, _lib.stream_of(dev))
+        _lib.check(st, h)
+        self._count(h)
+        c = list(counts)
+        return sxyz, sq, sgid, rxyz, rgid, c[:nranks], c[nranks:]
+
+    def dist_sort(self, src, q, sgid, recv, rgid, level):
+        dev = _lib.device_of(src.device)
+        h = _lib.handle(dev)
+        n, m = int(src.shape[0]), int(recv.shape[0])
+        words = max(1, (8 ** level) // 64)
+        bmp = torch.empty(2 * words, dtype=torch.int64, device=dev)
+        alloc = _lib.Allocator(dev)
+        so, ro = _lib.PointSetC(), _lib.PointSetC()
+        p = lambda t: t.data_ptr() if (t is not None and t.numel()) else None  # noqa: E731
+        st = _lib.load().fmmb_dist_sort(
+            h, p(src), p(q), n, p(sgid), p(recv), m, p(rgid), level, alloc.fn, None,
+            C.byref(so), C.byref(ro), bmp.data_ptr(), _lib.stream_of(dev))
+        if alloc.error is not None:
+            raise alloc.error
+        _lib.check(st, h)
+        self._count(h)
+        return (_point_set_from_c(so, alloc, level, q is not None),
+                _point_set_from_c(ro, alloc, level, False), bmp)
+
+    def dist_lists(self, gbmp, level, key_lo, key_hi):
+        dev = _lib.device_of(gbmp.device)
+        h = _lib.handle(dev)
+        alloc = _lib.Allocator(dev)
+        out = _lib.StructuresC()
+        st = _lib.load().fmmb_dist_lists(h, gbmp.data_ptr(), level, key_lo, key_hi, alloc.fn,
+                                         None, C.byref(out), _lib.stream_of(dev))
+        if alloc.error is not None:
+            raise alloc.error
+        _lib.check(st, h)
+        self._count(h)
+        L = level
+        rows_L = int(out.recv.k)
+        v = _lib.view
+        dsrc, drecv, sb, sr, sc = {}, {}, {}, {}, {}
+        rows = {L: rows_L}
+        for l in range(2, L):
+            dsrc[l] = v(alloc, out.dir_src[l], int(out.n_dir_src[l]), "u8")
+            drecv[l] = v(alloc, out.dir_recv[l], int(out.n_dir_recv[l]), "u8")
+            rows[l] = int(out.n_dir_recv[l])
+        for l in range(2, L + 1):
+            sb[l] = v(alloc, out.st_bookmark[l], rows[l] + 1, "i8")
+            sr[l] = v(alloc, out.st_ranks[l], int(out.n_st[l]), "i8")
+            sc[l] = v(alloc, out.st_codes[l], int(out.n_st[l]), "i2")
+        return DistLists(
+            neighbor_bookmark=v(alloc, out.neighbor_bookmark, rows_L + 1, "i8"),
+            neighbor_list=v(alloc, out.neighbor_list, int(out.n_neighbor), "i8"),
+            dir_src=dsrc, dir_recv=drecv, st_bookmark=sb, st_ranks=sr, st_codes=sc)
+
+
+# ------------------------------------------------------------ partition
+def partition_bits(level: int) -> int:
+    """Histogram resolution of the cut: the top min(14, 3L) key bits."""
+    return min(14, 3 * level)
+
+
+def cut_bins(hist: torch.Tensor, nranks: int) -> torch.Tensor:
+    """Rank of every histogram bin: contiguous bin ranges with balanced point
+    counts, rank(b) = min(P-1, floor(P * points-before-b / total)).  A pure
+    function of the all-reduced histogram, so every rank computes the same."""
+    h = hist.to(torch.int64)
+    excl = torch.cumsum(h, 0) - h
+    tot = int(h.sum())
+    if tot == 0:
+        return torch.zeros_like(h)
+    return torch.clamp((excl * nranks) // tot, max=nranks - 1)
+
+
+def key_windows(bin_rank: torch.Tensor, nranks: int, level: int, pbits: int) -> list:
+    """[key_lo, key_hi) of every rank's level-L key range."""
+    br = bin_rank.cpu()
+    nb = br.numel()
+    sh = 3 * level - pbits
+    starts = torch.searchsorted(br, torch.arange(nranks + 1, dtype=br.dtype)).tolist()
+    starts[-1] = nb
+    return [(starts[g] << sh, starts[g + 1] << sh) for g in range(nranks)]
+
+
+# ----------------------------------------------------------------- driver
+@dataclass
+class DistShard:
+    """One rank's contiguous shard of every FmmStructures array (global
+    offsets applied; the CSR/bookmark trailing entry only on the last rank)."""
+
+    rank: int
+    nranks: int
+    max_level: int
+    key_window: tuple
+    sorted_src: SortedPointSet
+    sorted_recv: SortedPointSet
+    neighbor_table: NeighborTable
+    directory: LevelDirectory
+    stencils: TranslationStencils
+    exchanged: dict = field(default_factory=dict)  # points sent to other ranks
+
+    def to_numpy(self) -> "DistShard":
+        """Host copy of the shard (numpy arrays, reference dtypes)."""
+        def npy(v):
+            return v.cpu().numpy() if isinstance(v, torch.Tensor) else v
+
+        def ps(p):
+            return SortedPointSet(level=p.level, points=npy(p.points), charges=npy(p.charges),
+                                  permutation=npy(p.permutation), bookmarks=npy(p.bookmarks),
+                                  non_empty_index=npy(p.non_empty_index), boxes=npy(p.boxes))
+
+        d, st = self.directory, self.stencils
+        return DistShard(
+            rank=self.rank, nranks=self.nranks, max_level=self.max_level,
+            key_window=self.key_window, sorted_src=ps(self.sorted_src),
+            sorted_recv=ps(self.sorted_recv),
+            neighbor_table=NeighborTable(npy(self.neighbor_table.neighbor_bookmark),
+                                         npy(self.neighbor_table.neighbor_list)),
+            directory=LevelDirectory(d.max_level, {l: npy(v) for l, v in d.src_boxes.items()},
+                                     {l: npy(v) for l, v in d.recv_boxes.items()}),
+            stencils=TranslationStencils({l: npy(v) for l, v in st.bookmark.items()},
+                                         {l: npy(v) for l, v in st.ranks.items()},
+                                         {l: npy(v) for l, v in st.codes.items()}),
+            exchanged=dict(self.exchanged))
+
+
+def _shard_csr(bm: torch.Tensor, offset: int, last: bool) -> torch.Tensor:
+    x = bm + offset
+    return x if last else x[:-1]
+
+
+def build_all_distributed(shards: list, max_level: int, comm: Comm, ops=None,
+                          pbits: int | None = None) -> list:
+    """Partitioned build.  `shards[i] = (src, charges, recv)` of the rank
+    comm.ranks[i]: device tensors, index-contiguous pieces of the global
+    arrays in rank order.  Returns one DistShard per driven rank."""
+    check_level(max_level)
+    if max_level < 2:
+        raise DomainError("the partitioned build needs max_level >= 2")
+    ops = ops or DeviceOps()
+    L = max_level
+    P = comm.size
+    pb = pbits or partition_bits(L)
+    nd = len(comm.ranks)
+    dev = [s[0].device for s in shards]
+    # 1. global index bases
+    sizes = [torch.tensor([int(s[0].shape[0]), int(s[2].shape[0])], dtype=torch.int64,
+                          device=dev[i]) for i, s in enumerate(shards)]
+    allsz = [[int(v) for t in g for v in t.cpu().tolist()] for g in comm.all_gather(sizes)]
+    gb = []
+    for i, r in enumerate(comm.ranks):
+        ns, ms = allsz[i][0::2], allsz[i][1::2]
+        gb.append((sum(ns[:r]), sum(ms[:r])))
+    # 2. histogram -> cut
+    hists = [ops.part_histogram(s[0], s[2], L, pb) for s in shards]
+    hists = comm.allreduce_sum(hists)
+    bin_rank = cut_bins(hists[0], P)
+    windows = key_windows(bin_rank, P, L, pb)
+    # 3. pack + exchange
+    packs = [ops.part_pack(s[0], s[1], s[2], L, pb, bin_rank, P, gb[i][0], gb[i][1])
+             for i, s in enumerate(shards)]
+
+    def split(t, cnts):
+        out, at = [], 0
+        for c in cnts:
+            out.append(t[at: at + c])
+            at += c
+        return out
+
+    with_q = shards[0][1] is not None
+    ex = {}
+    for key, idx, cidx in (("sxyz", 0, 5), ("sgid", 2, 5), ("rxyz", 3, 6), ("rgid", 4, 6)):
+        ex[key] = comm.all_to_all([split(pk[idx], pk[cidx]) for pk in packs])
+    if with_q:
+        ex["sq"] = comm.all_to_all([split(pk[1], pk[5]) for pk in packs])
+    results = []
+    sorted_sets = []
+    bmps = []
+    for i, r in enumerate(comm.ranks):
+        src = torch.cat(ex["sxyz"][i]) if ex["sxyz"][i] else torch.empty((0, 3), dtype=torch.float64, device=dev[i])
+        sgid = torch.cat(ex["sgid"][i])
+        rxyz = torch.cat(ex["rxyz"][i])
+        rgid = torch.cat(ex["rgid"][i])
+        q = torch.cat(ex["sq"][i]) if with_q else None
+        sent = sum(int(t.shape[0]) for d, t in enumerate(split(packs[i][0], packs[i][5])) if d != r)
+        sent_r = sum(int(t.shape[0]) for d, t in enumerate(split(packs[i][3], packs[i][6])) if d != r)
+        # 4. local sort phase
+        ss, sr, bmp = ops.dist_sort(src, q, sgid, rxyz, rgid, L)
+        sorted_sets.append((ss, sr))
+        bmps.append(bmp)
+        results.append({"sent_points": sent + sent_r})
+    # 5. global occupancy
+    gbmps = comm.allreduce_sum(bmps)
+    # 6. owned lists
+    lists = [ops.dist_lists(gbmps[i], L, *windows[r]) for i, r in enumerate(comm.ranks)]
+    # 7. global offsets from every rank's shard sizes
+    def stats(i):
+        ss, sr = sorted_sets[i]
+        dl = lists[i]
+        v = [ss.points.shape[0], sr.points.shape[0], dl.neighbor_bookmark[-1]]
+        for l in range(2, L + 1):
+            v.append(dl.st_bookmark[l][-1])
+        return torch.tensor([int(x) for x in v], dtype=torch.int64, device=dev[i])
+
+    allst = comm.all_gather([stats(i) for i in range(nd)])
+    out = []
+    for i, r in enumerate(comm.ranks):
+        st = torch.stack([t.cpu() for t in allst[i]])  # (P, 3 + L - 1)
+        before = st[:r].sum(0) if r else torch.zeros(st.shape[1], dtype=torch.int64)
+        last = r == P - 1
+        ss, sr = sorted_sets[i]
+        dl = lists[i]
+        ss.bookmarks = _shard_csr(ss.bookmarks, int(before[0]), last)
+        sr.bookmarks = _shard_csr(sr.bookmarks, int(before[1]), last)
+        nt = NeighborTable(_shard_csr(dl.neighbor_bookmark, int(before[2]), last),
+                           dl.neighbor_list)
+        dsrc = {L: ss.non_empty_index, **dl.dir_src}
+        drecv = {L: sr.non_empty_index, **dl.dir_recv}
+        sb = {l: _shard_csr(dl.st_bookmark[l], int(before[3 + l - 2]), last)
+              for l in range(2, L + 1)}
+        out.append(DistShard(
+            rank=r, nranks=P, max_level=L, key_window=windows[r], sorted_src=ss,
+            sorted_recv=sr, neighbor_table=nt, directory=LevelDirectory(L, dsrc, drecv),
+            stencils=TranslationStencils(sb, dl.st_ranks, dl.st_codes), exchanged=results[i]))
+    return out
+
+
+def concat_shards(shards: list) -> FmmStructures:
+    """The global FmmStructures from every rank's shard (rank order)."""
+    shards = sorted(shards, key=lambda s: s.rank)
+    L = shards[0].max_level
+
+    def cat(get):
+        parts = [get(s) for s in shards]
+        if isinstance(parts[0], torch.Tensor):
+            return torch.cat([p.to(parts[0].device) for p in parts])
+        return np.concatenate(parts)
+
+    def ps(side):
+        first = getattr(shards[0], side)
+        return SortedPointSet(
+            level=L,
+            points=cat(lambda s: getattr(s, side).points),
+            charges=None if first.charges is None else cat(lambda s: getattr(s, side).charges),
+            permutation=cat(lambda s: getattr(s, side).permutation),
+            bookmarks=cat(lambda s: getattr(s, side).bookmarks),
+            non_empty_index=cat(lambda s: getattr(s, side).non_empty_index),
+            boxes=cat(lambda s: getattr(s, side).boxes))
+
+    levels = range(2, L + 1)
+    return FmmStructures(
+        max_level=L, sorted_src=ps("sorted_src"), sorted_recv=ps("sorted_recv"),
+        neighbor_table=NeighborTable(cat(lambda s: s.neighbor_table.neighbor_bookmark),
+                                     cat(lambda s: s.neighbor_table.neighbor_list)),
+        directory=LevelDirectory(
+            L, {l: cat(lambda s: s.directory.src_boxes[l]) for l in levels},
+            {l: cat(lambda s: s.directory.recv_boxes[l]) for l in levels}),
+        stencils=TranslationStencils(
+            {l: cat(lambda s: s.stencils.bookmark[l]) for l in levels},
+            {l: cat(lambda s: s.stencils.ranks[l]) for l in levels},
+            {l: cat(lambda s: s.stencils.codes[l]) for l in levels}))
