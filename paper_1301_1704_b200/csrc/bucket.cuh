@@ -141,10 +141,10 @@ __global__ void __launch_bounds__(kHThreads)
 // ------------------------------------------------------------- scan pass --
 // CTA = kScanBuckets buckets in order (ticket + decoupled look-back).
 // bstart[b] = first sorted position of bucket b (bstart[nb] = n + m),
-// cursor[b] = bstart[b], *maxb = largest bucket.
+// *maxb = largest bucket.
 __global__ void __launch_bounds__(256)
     k_bkt_scan(const uint32_t* __restrict__ mat, const BucketGeo g, uint32_t* __restrict__ bstart,
-               uint32_t* __restrict__ cursor, uint64_t* __restrict__ states,
+               uint64_t* __restrict__ states,
                uint32_t* __restrict__ ticket, uint32_t* __restrict__ maxb) {
   constexpr int kPer = kScanBuckets / 256;
   __shared__ uint32_t s_w[8];
@@ -194,11 +194,184 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
   for (int e = 0; e < kPer; ++e) {
     const int b = b0 + e;
-    if (b < g.nb) {
-      bstart[b] = run;
-      cursor[(size_t)b * kCursorStride] = run;
-    }
+    if (b < g.nb) bstart[b] = run;
     run += c[e];
+  }
+}
+
+// ------------------------------------------------------- refinement ----
+// Skewed inputs (a coarse bucket holds more points than the local sort's
+// shared memory) are handled by splitting every such bucket along the next
+// kRefBits key bits: a fine histogram of the big buckets' points, then a
+// greedy grouping of consecutive sub-bins into FINAL buckets of <= kLcCap
+// points.  A final bucket is a contiguous key range [lo, lo + span); uniform
+// inputs keep final == coarse buckets (nothing is refined).
+constexpr int kRefBits = 8;
+constexpr int kLcSmallBits_ = 11;  // = kLcSmallBits (box-count path span)
+constexpr int kRefBins = 1 << kRefBits;
+
+struct BDesc {          // final bucket: level-L key range and set
+  uint64_t lo;
+  uint64_t span_set;    // span | set << 63
+};
+
+__host__ inline int64_t final_buckets_cap(const BucketGeo& g, int64_t cap) {
+  // greedy groups: two neighbours hold > cap points or a neighbour is a full
+  // run of sub-bins, so groups <= 2 * points / cap + 2 * runs + 1 per bucket
+  const int R = g.shift < kRefBits ? g.shift : kRefBits;
+  const int sh_sub = g.shift - R;
+  const int64_t runs = sh_sub >= 11 ? (1 << R) : ((1 << R) >> (11 - sh_sub));
+  return (int64_t)g.nb * (1 + 2 * std::max<int64_t>(runs, 1)) + 3 * ((g.n + g.m) / cap + 1);
+}
+
+__device__ __forceinline__ int ref_bits(const BucketGeo& g) {
+  return g.shift < kRefBits ? g.shift : kRefBits;
+}
+
+// a coarse bucket is refined when it holds more points than the local sort's
+// shared memory, or when its key span is too wide for the box-count path
+// (then final buckets are also capped at 2^kLcSmallBits keys)
+__device__ __forceinline__ bool wide_buckets(const BucketGeo& g) {
+  return g.shift > kLcSmallBits_;
+}
+__device__ __forceinline__ bool needs_refine(const BucketGeo& g, uint32_t count, uint32_t cap) {
+  return count > cap || (wide_buckets(g) && count > 0);
+}
+
+// fine histogram of the points of over-full coarse buckets (a no-op grid when
+// every bucket fits)
+template <bool NARROW>
+__global__ void __launch_bounds__(256)
+    k_bkt_fine(const double* __restrict__ src, const double* __restrict__ recv,
+               const BucketGeo g, int level, const uint32_t* __restrict__ bstart,
+               const uint32_t* __restrict__ maxb, uint32_t cap, uint32_t* __restrict__ fine) {
+  if (__ldg(maxb) <= cap && !wide_buckets(g)) return;
+  const int64_t tot = g.n + g.m;
+  const uint64_t kmask = (1ull << g.sbits) - 1ull;
+  const double grid = (double)(1ll << level);
+  const int R = ref_bits(g);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double* p = row_ptr(src, recv, g.n, i);
+    const uint64_t key = encode_any<NARROW>(__ldg(p), __ldg(p + 1), __ldg(p + 2), level, grid) & kmask;
+    const uint32_t b = bucket_of(key, i >= g.n, g);
+    if (needs_refine(g, __ldg(bstart + b + 1) - __ldg(bstart + b), cap)) {
+      const uint32_t sub = (uint32_t)((key >> (g.shift - R)) & ((1u << R) - 1u));
+      atomicAdd(fine + (size_t)b * kRefBins + sub, 1u);
+    }
+  }
+}
+
+// Final buckets: thread per coarse bucket (CTA = 256 buckets, tickets +
+// decoupled look-back for the final-bucket numbering).  Writes fbase[b],
+// the sub-bin -> group table of refined buckets, every final bucket's start,
+// descriptor and scatter cursor, and nfinal.
+struct PlanOut {
+  uint32_t* fbase;   // [nb]
+  uint8_t* gtab;     // [nb * kRefBins]
+  uint32_t* bstart_f;  // [nfinal + 1]
+  BDesc* desc;       // [nfinal]
+  uint32_t* cursor;  // [nfinal * kCursorStride]
+  uint32_t* nfinal;  // [1]
+  uint32_t* fail;    // [1]
+  uint64_t* states;  // [nb / 256 + 1]
+  uint32_t* ticket;  // [1]
+};
+
+__global__ void __launch_bounds__(256)
+    k_bkt_plan(const BucketGeo g, const uint32_t* __restrict__ bstart,
+               const uint32_t* __restrict__ maxb, uint32_t cap,
+               const uint32_t* __restrict__ fine, const PlanOut o) {
+  __shared__ uint32_t s_w[8];
+  __shared__ int64_t s_tile, s_base;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) s_tile = atomicAdd(o.ticket, 1u);
+  __syncthreads();
+  const int64_t tile = s_tile;
+  const int b = (int)tile * 256 + tid;
+  const bool refined = __ldg(maxb) > cap || wide_buckets(g);
+  const int R = ref_bits(g);
+  const int nsub = 1 << R;
+  // sub-bins per final bucket: its key span stays within the count path
+  const int sh_sub = g.shift - R;
+  const int max_run = sh_sub >= kLcSmallBits_ ? 1 : (1 << (kLcSmallBits_ - sh_sub));
+  uint32_t c = 0, ns = 0;
+  if (b < g.nb) {
+    c = bstart[b + 1] - bstart[b];
+    ns = 1;
+    if (refined && needs_refine(g, c, cap)) {  // greedy groups of consecutive sub-bins
+      const uint32_t* f = fine + (size_t)b * kRefBins;
+      uint32_t acc = 0, grp = 0;
+      int run = 0;
+      for (int sb = 0; sb < nsub; ++sb) {
+        const uint32_t v = f[sb];
+        if (v > cap) atomicOr(o.fail, 1u);
+        if ((acc + v > cap && acc > 0) || run == max_run) {
+          ++grp;
+          acc = 0;
+          run = 0;
+        }
+        acc += v;
+        ++run;
+        o.gtab[(size_t)b * kRefBins + sb] = (uint8_t)grp;
+      }
+      ns = grp + 1;
+    }
+  }
+  uint32_t wt;
+  uint32_t x = warp_excl_scan(ns, wt);
+  if (lane == 0) s_w[warp] = wt;
+  __syncthreads();
+  uint32_t all = 0;
+  for (int i = 0; i < 8; ++i) {
+    x += i < warp ? s_w[i] : 0u;
+    all += s_w[i];
+  }
+  if (tid == 0) {
+    uint64_t* st = o.states + tile;
+    uint64_t excl = 0;
+    if (tile == 0) {
+      st_state(st, kStInclusive | all);
+    } else {
+      st_state(st, kStAggregate | all);
+      excl = lookback(o.states, tile, 0, 1);
+      st_state(st, kStInclusive | (excl + all));
+    }
+    s_base = (int64_t)excl;
+    if ((int64_t)(tile + 1) * 256 >= g.nb) {
+      *o.nfinal = (uint32_t)(excl + all);
+      o.bstart_f[excl + all] = (uint32_t)(g.n + g.m);
+    }
+  }
+  __syncthreads();
+  if (b >= g.nb) return;
+  const uint32_t fb = (uint32_t)s_base + x;
+  o.fbase[b] = fb;
+  const uint64_t set = (uint64_t)(b >> g.bb);
+  const uint64_t lo = (uint64_t)(b & ((1 << g.bb) - 1)) << g.shift;
+  if (ns == 1) {
+    o.bstart_f[fb] = bstart[b];
+    o.desc[fb] = BDesc{lo, (1ull << g.shift) | (set << 63)};
+    o.cursor[(size_t)fb * kCursorStride] = bstart[b];
+    return;
+  }
+  const uint32_t* f = fine + (size_t)b * kRefBins;
+  const int sh = g.shift - R;
+  uint32_t start = bstart[b];
+  int first = 0;
+  for (int sb = 0; sb <= nsub; ++sb) {
+    const bool end = sb == nsub || o.gtab[(size_t)b * kRefBins + sb] !=
+                                       o.gtab[(size_t)b * kRefBins + first];
+    if (end) {
+      const uint32_t fid = fb + o.gtab[(size_t)b * kRefBins + first];
+      uint32_t cnt = 0;
+      for (int k = first; k < sb; ++k) cnt += f[k];
+      o.bstart_f[fid] = start;
+      o.desc[fid] = BDesc{lo + ((uint64_t)first << sh), ((uint64_t)(sb - first) << sh) | (set << 63)};
+      o.cursor[(size_t)fid * kCursorStride] = start;
+      start += cnt;
+      first = sb;
+    }
   }
 }
 
@@ -269,12 +442,19 @@ __host__ inline int64_t scatter_rows_per_cta(int64_t tot, int grid) {
   return ((r + kSRows - 1) / kSRows) * kSRows;
 }
 
+struct FinalMap {  // coarse bucket (+ next kRefBits key bits) -> final bucket
+  const uint32_t* fbase;
+  const uint8_t* gtab;
+  const uint32_t* maxb;
+  uint32_t cap;
+};
+
 template <bool NARROW>
 __global__ void __launch_bounds__(kSThreads, 1)
     k_bkt_scatter(const double* __restrict__ src, const double* __restrict__ q,
                   const double* __restrict__ recv, const BucketGeo g, int level,
                   int64_t cta_rows, uint32_t* __restrict__ cursor, double* __restrict__ rec,
-                  uint32_t* __restrict__ idx) {
+                  uint32_t* __restrict__ idx, const FinalMap fm) {
   extern __shared__ __align__(128) unsigned char sc_smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(sc_smem + (size_t)kSStages * kSStageBytes);
   uint64_t* empty = full + kSStages;
@@ -295,6 +475,8 @@ __global__ void __launch_bounds__(kSThreads, 1)
   __syncthreads();
   const uint64_t kmask = (1ull << g.sbits) - 1ull;
   const double grid = (double)(1ll << level);
+  const bool refined = __ldg(fm.maxb) > fm.cap || wide_buckets(g);
+  const int R = ref_bits(g);
   auto stage_xyz = [&](int k) {
     return reinterpret_cast<double*>(sc_smem + (size_t)(k % kSStages) * kSStageBytes);
   };
@@ -342,9 +524,12 @@ __global__ void __launch_bounds__(kSThreads, 1)
       xyz[3 * tid + 2] = __ldg(p + 2);
       if (i < n) xyz[3 * kSRows + tid] = q ? __ldg(q + i) : 0.0;
     }
-    const uint32_t b = bucket_of(
-        encode_any<NARROW>(xyz[3 * tid], xyz[3 * tid + 1], xyz[3 * tid + 2], level, grid) & kmask,
-        i >= n, g);
+    const uint64_t key =
+        encode_any<NARROW>(xyz[3 * tid], xyz[3 * tid + 1], xyz[3 * tid + 2], level, grid) & kmask;
+    uint32_t b = bucket_of(key, i >= n, g);
+    if (refined)
+      b = __ldg(fm.fbase + b) +
+          __ldg(fm.gtab + (size_t)b * kRefBins + ((key >> (g.shift - R)) & ((1u << R) - 1u)));
     return atomicAdd(cursor + (size_t)b * kCursorStride, 1u);
   };
   auto store = [&](int k, uint32_t dst) {
@@ -492,9 +677,10 @@ __device__ __forceinline__ int64_t perm_of(const LocalOut& o, int set, int64_t l
 template <typename CK, bool NARROW, bool HEADS>
 __global__ void __launch_bounds__(kLcThreads)
     k_bkt_local(const double* __restrict__ rec, uint32_t* __restrict__ idx,
-                const uint32_t* __restrict__ bstart, const BucketGeo g, int level,
-                const LocalOut o, uint64_t* __restrict__ states, uint32_t* __restrict__ ticket,
-                const uint32_t* __restrict__ maxb, uint32_t* __restrict__ fail) {
+                const uint32_t* __restrict__ bstart, const BDesc* __restrict__ desc,
+                const uint32_t* __restrict__ nfinal, const BucketGeo g, int level,
+                const LocalOut o, uint64_t* __restrict__ states,
+                const uint32_t* __restrict__ fail) {
   extern __shared__ __align__(128) unsigned char lc_smem[];
   double* s_rec = reinterpret_cast<double*>(lc_smem);                   // [cap][4]
   uint32_t* s_idx = reinterpret_cast<uint32_t*>(s_rec + 4 * kLcCap);    // [cap]
@@ -507,29 +693,42 @@ __global__ void __launch_bounds__(kLcThreads)
   uint32_t* s_red = reinterpret_cast<uint32_t*>(s_misc + 4);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  if (__ldg(maxb) > (uint32_t)kLcCap) {  // some bucket overflows: general path
-    if (blockIdx.x == 0 && tid == 0) atomicOr(fail, 1u);
-    return;
-  }
+  if (__ldg(fail)) return;  // a final bucket overflows: the host reruns on the general path
   uint64_t* bar = s_misc + 2;
   if (tid == 0) {
-    s_misc[0] = HEADS ? (uint64_t)blockIdx.x : (uint64_t)atomicAdd(ticket, 1u);
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int64_t tile = (int64_t)s_misc[0];
-  const int b = (int)tile;
-  const int64_t bs = bstart[b];
-  const int B = (int)(bstart[b + 1] - bs);
-  const int set = b >> g.bb;
-  const uint64_t prefix = (uint64_t)(b & ((1 << g.bb) - 1)) << g.shift;
-  const uint64_t lmask = (1ull << g.shift) - 1ull;
+  const uint32_t nf = __ldg(nfinal);
+  uint32_t bar_phase = 0;
   const int64_t n = g.n, m = g.m, tot = n + m;
+  // persistent: every resident CTA walks the final buckets round-robin (in
+  // order, so the non-HEADS look-back always finds its predecessors running)
+  for (int64_t tile = blockIdx.x; tile < nf; tile += gridDim.x) {
+  const int64_t bs = bstart[tile];
+  const int B = (int)(bstart[tile + 1] - bs);
+  const BDesc d = desc[tile];
+  const int set = (int)(d.span_set >> 63);
+  const uint64_t span = d.span_set & ~(1ull << 63);
+  const uint64_t prefix = d.lo;  // first level-L key of the bucket; lk = key - lo
+  if (B == 0) {  // empty final bucket: nothing to write (the look-back still needs its state)
+    if (!HEADS && tid == 0) {
+      uint64_t* st = states + tile;
+      if (tile == 0) {
+        st_state(st, kStInclusive);
+      } else {
+        st_state(st, kStAggregate);
+        st_state(st, kStInclusive | lookback(states, tile, 0, 1));
+      }
+    }
+    continue;
+  }
 
   // phase 0: bulk copy of the bucket's records (TMA), source indices by LDG
   if (tid == 0 && B > 0) {
     const uint32_t bytes = (uint32_t)B * 32u;
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
                  "r"(bytes)
                  : "memory");
@@ -542,21 +741,15 @@ __global__ void __launch_bounds__(kLcThreads)
   if (set == 0)
     for (int j = tid; j < B; j += kLcThreads) s_idx[j] = __ldg(idx + bs + j);
   if (B > 0) {
-    uint32_t done = 0;
-    while (!done)
-      asm volatile(
-          "{\n\t.reg .pred p;\n\tmbarrier.try_wait.parity.shared::cta.b64 p, [%1], 0;\n\t"
-          "selp.u32 %0, 1, 0, p;\n\t}"
-          : "=r"(done)
-          : "r"(smem_u32(bar))
-          : "memory");
+    mbar_wait(bar, bar_phase);
+    bar_phase ^= 1u;
   }
   __syncthreads();
   // phase 1: low key bits and combined input index of every record; with
   // HEADS and <= 2^12 boxes per bucket also the per-box counts
   const double grid = (double)(1ll << level);
-  const bool small = HEADS && g.shift <= kLcSmallBits;
-  const int nbins = 1 << (g.shift <= kLcSmallBits ? g.shift : 0);
+  const bool small = HEADS && span <= (1ull << kLcSmallBits);
+  const int nbins = small ? (int)span : 1;
   if (small)
     for (int i = tid; i < nbins; i += kLcThreads) s_wh[i] = 0;
   __syncthreads();
@@ -564,13 +757,13 @@ __global__ void __launch_bounds__(kLcThreads)
     const double* r = s_rec + 4 * j;
     const uint64_t key = encode_any<NARROW>(r[0], r[1], r[2], level, grid);
     const uint32_t ci = set == 0 ? s_idx[j] : (uint32_t)(n + __double_as_longlong(r[3]));
-    const uint32_t lk = (uint32_t)(key & lmask);
+    const uint64_t lk = key - prefix;  // < span
     if (small) {
       k0[j] = (CK)lk;
       s_idx[j] = ci;
-      atomicAdd(&s_wh[lk], 1u);
+      atomicAdd(&s_wh[(uint32_t)lk], 1u);
     } else {
-      k0[j] = ((CK)(key & lmask) << g.cbits) | (CK)ci;
+      k0[j] = ((CK)lk << g.cbits) | (CK)ci;
     }
     p0[j] = (uint16_t)j;
   }
@@ -614,7 +807,7 @@ __global__ void __launch_bounds__(kLcThreads)
       if (i < nbins) {
         s_wh[i] = (c[e] << 16) | start;
         if (c[e]) {
-          const uint64_t mk = prefix | (uint64_t)i;
+          const uint64_t mk = prefix + (uint64_t)i;
           if (bm) atomicOr(bm + (mk >> 6), 1ull << (mk & 63));
           hp[hidx] = (uint32_t)(bs + start - (set ? n : 0));
           ++hidx;
@@ -666,14 +859,17 @@ __global__ void __launch_bounds__(kLcThreads)
       } else {
         o.perm[p] = perm_of(o, 1, __double_as_longlong(r[3]));
       }
-      o.boxes[p] = prefix | (uint64_t)k0[j];
+      o.boxes[p] = prefix + (uint64_t)k0[j];
     }
-    return;
+    __syncthreads();  // smem reused by the next bucket
+    continue;
   }
   // phase 2: LSD passes over the composite (index bits first, then key bits)
   CK* kc = k0;
   uint16_t* pc = p0;
-  const int cbits = g.shift + g.cbits;
+  int lbits = 0;
+  while (lbits < 63 && (1ull << lbits) < span) ++lbits;
+  const int cbits = lbits + g.cbits;
   for (int ds = 0; ds < cbits; ds += kLcDigit) {
     const int db = cbits - ds < kLcDigit ? cbits - ds : kLcDigit;
     CK* ko = kc == k0 ? k1 : k0;
@@ -736,7 +932,7 @@ __global__ void __launch_bounds__(kLcThreads)
       const int64_t p = bs + j;  // combined sorted position
       const int pl = pc[j];
       const double* r = s_rec + 4 * pl;
-      const uint64_t mk = prefix | lk;
+      const uint64_t mk = prefix + lk;
       double* po = o.pts + 3 * p;
       po[0] = r[0];
       po[1] = r[1];
@@ -778,6 +974,7 @@ __global__ void __launch_bounds__(kLcThreads)
     hbase += ctot;
     __syncthreads();  // s_red[8..] reused by the next chunk
   }
+  }  // final buckets
 }
 
 // Bookmarks and non-empty keys at their global box ranks (HEADS variant):
@@ -797,47 +994,52 @@ struct HeadsParams {
 };
 
 __global__ void __launch_bounds__(256)
-    k_bkt_heads(const __grid_constant__ HeadsParams hp, const BucketGeo g) {
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int b = blockIdx.x * 8 + warp;
+    k_bkt_heads(const __grid_constant__ HeadsParams hp, const BDesc* __restrict__ desc,
+                const uint32_t* __restrict__ nfinal, const BucketGeo g) {
+  const int lane = threadIdx.x & 31;
   const int64_t ks = *hp.ktot_src;
-  if (b == 0 && lane == 0) {
+  const int64_t gw = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (gw == 0 && lane == 0) {
     const int64_t kr = *hp.ktot_recv;
     hp.bm[ks] = g.n;
     hp.bm[ks + 1 + kr] = g.m;
     hp.kinfo[0] = ks;
     hp.kinfo[1] = ks + kr;
   }
-  if (b >= g.nb) return;
-  const int set = b >> g.bb;
-  const uint64_t key0 = (uint64_t)(b & ((1 << g.bb) - 1)) << g.shift;
-  const uint64_t nbits = 1ull << g.shift;
-  const uint64_t* bmp = set ? hp.bmp[1] : hp.bmp[0];
-  const uint32_t* dir = set ? hp.dir[1] : hp.dir[0];
-  const uint32_t* hpos = hp.hpos + hp.bstart[b];
-  uint64_t* ne = hp.ne + (set ? ks : 0);
-  int64_t* bm = hp.bm + (set ? ks + 1 : 0);
-  const int64_t w0 = (int64_t)(key0 >> 6);
-  const uint64_t below0 = (key0 & 63) ? (__ldg(bmp + w0) & ((1ull << (key0 & 63)) - 1ull)) : 0ull;
-  const int64_t rank0 = (int64_t)__ldg(dir + w0) + __popcll(below0);
+  const uint32_t nf = __ldg(nfinal);
   const unsigned lt = lanemask_lt();
-  int64_t h = 0;
-  // lane = box: 32 consecutive keys per step; all-zero 64-bit words skipped
-  for (uint64_t off = 0; off < nbits; off += 32) {
-    const uint64_t key = key0 + off + lane;
-    const uint64_t word = __ldg(bmp + (key >> 6));
-    if (__all_sync(0xffffffffu, word == 0)) {  // skip the rest of an empty word
-      off = ((key0 + off + 64) & ~63ull) - key0 - 32;
-      continue;
+  for (int64_t f = gw; f < nf; f += (int64_t)gridDim.x * 8) {
+    if (hp.bstart[f + 1] == hp.bstart[f]) continue;  // empty final bucket
+    const BDesc d = desc[f];
+    const int set = (int)(d.span_set >> 63);
+    const uint64_t nbits = d.span_set & ~(1ull << 63);
+    const uint64_t key0 = d.lo;
+    const uint64_t* bmp = set ? hp.bmp[1] : hp.bmp[0];
+    const uint32_t* dir = set ? hp.dir[1] : hp.dir[0];
+    const uint32_t* hpos = hp.hpos + hp.bstart[f];
+    uint64_t* ne = hp.ne + (set ? ks : 0);
+    int64_t* bm = hp.bm + (set ? ks + 1 : 0);
+    const int64_t w0 = (int64_t)(key0 >> 6);
+    const uint64_t below0 = (key0 & 63) ? (__ldg(bmp + w0) & ((1ull << (key0 & 63)) - 1ull)) : 0ull;
+    const int64_t rank0 = (int64_t)__ldg(dir + w0) + __popcll(below0);
+    int64_t h = 0;
+    // lane = box: 32 consecutive keys per step; all-zero 64-bit words skipped
+    for (uint64_t off = 0; off < nbits; off += 32) {
+      const uint64_t key = key0 + off + lane;
+      const uint64_t word = __ldg(bmp + (key >> 6));
+      if (__all_sync(0xffffffffu, word == 0)) {  // skip the rest of an empty word
+        off = ((key0 + off + 64) & ~63ull) - key0 - 32;
+        continue;
+      }
+      const bool occ = off + lane < nbits && ((word >> (key & 63)) & 1ull);
+      const unsigned ballot = __ballot_sync(0xffffffffu, occ);
+      if (occ) {
+        const int64_t at = h + __popc(ballot & lt);
+        ne[rank0 + at] = key;
+        bm[rank0 + at] = (int64_t)__ldg(hpos + at);
+      }
+      h += __popc(ballot);
     }
-    const bool occ = off + lane < nbits && ((word >> (key & 63)) & 1ull);
-    const unsigned ballot = __ballot_sync(0xffffffffu, occ);
-    if (occ) {
-      const int64_t at = h + __popc(ballot & lt);
-      ne[rank0 + at] = key;
-      bm[rank0 + at] = (int64_t)__ldg(hpos + at);
-    }
-    h += __popc(ballot);
   }
 }
 

@@ -184,29 +184,39 @@ struct BuildPlanHost {  // mirrored in the pinned readback block
 struct BucketRun {  // scratch that outlives the sort phase (heads pass)
   char* scratch = nullptr;
   BucketGeo g{};
-  const uint32_t* bstart = nullptr;
+  const uint32_t* bstart_f = nullptr;
+  const BDesc* desc = nullptr;
+  const uint32_t* nfinal = nullptr;
   const uint32_t* hpos = nullptr;
 };
 
 template <typename CK, bool NARROW, bool HEADS>
-void launch_local(const double* rec, uint32_t* idx, const uint32_t* bstart, const BucketGeo& g,
-                  int L, const LocalOut& o, uint64_t* lst, uint32_t* ctl, uint32_t* fail,
-                  cudaStream_t s) {
-  k_bkt_local<CK, NARROW, HEADS><<<(unsigned)g.nb, kLcThreads, lc_smem_bytes<CK>(), s>>>(
-      rec, idx, bstart, g, L, o, lst, ctl + 1, ctl + 2, fail);
+void launch_local(fmmb_handle_t h, const double* rec, uint32_t* idx, const uint32_t* bstart_f,
+                  const BDesc* desc, const uint32_t* nfinal, const BucketGeo& g, int L,
+                  const LocalOut& o, uint64_t* lst, const uint32_t* fail, cudaStream_t s) {
+  auto kern = k_bkt_local<CK, NARROW, HEADS>;
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLcThreads, lc_smem_bytes<CK>());
+  const int grid = std::max(1, per_sm) * h->num_sms;  // persistent: all CTAs resident
+  kern<<<grid, kLcThreads, lc_smem_bytes<CK>(), s>>>(rec, idx, bstart_f, desc, nfinal, g, L, o,
+                                                     lst, fail);
 }
 
 template <bool NARROW>
 void launch_hs(const double* src, const double* q, const double* recv, const BucketGeo& g,
-               int num_sms, int L, uint32_t* mat, uint32_t* bstart, uint32_t* cursor, uint64_t* sst,
-               uint32_t* ctl, double* rec, uint32_t* idx, uint32_t* err, cudaStream_t s) {
+               int num_sms, int L, uint32_t* mat, uint32_t* bstart, uint64_t* sst, uint32_t* ctl,
+               uint32_t* fine, const PlanOut& po, double* rec, uint32_t* idx, uint32_t* err,
+               cudaStream_t s) {
   k_bkt_hist<NARROW><<<(unsigned)g.hgrid, kHThreads, (size_t)g.nb * 4, s>>>(src, recv, g, L,
                                                                              mat, err);
-  k_bkt_scan<<<(unsigned)ceil_div(g.nb, kScanBuckets), 256, 0, s>>>(mat, g, bstart, cursor, sst,
+  k_bkt_scan<<<(unsigned)ceil_div(g.nb, kScanBuckets), 256, 0, s>>>(mat, g, bstart, sst,
                                                                     ctl + 0, ctl + 2);
+  k_bkt_fine<NARROW><<<num_sms * 8, 256, 0, s>>>(src, recv, g, L, bstart, ctl + 2, kLcCap, fine);
+  k_bkt_plan<<<(unsigned)ceil_div(g.nb, 256), 256, 0, s>>>(g, bstart, ctl + 2, kLcCap, fine, po);
   const int sgrid = (int)std::min<int64_t>(num_sms, ceil_div(g.n + g.m, kSRows));
+  const FinalMap fm{po.fbase, po.gtab, ctl + 2, kLcCap};
   k_bkt_scatter<NARROW><<<(unsigned)sgrid, kSThreads, scatter_smem_bytes(), s>>>(
-      src, q, recv, g, L, scatter_rows_per_cta(g.n + g.m, sgrid), cursor, rec, idx);
+      src, q, recv, g, L, scatter_rows_per_cta(g.n + g.m, sgrid), po.cursor, rec, idx, fm);
 }
 
 fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int64_t n,
@@ -215,14 +225,21 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
                         BucketRun& run) {
   const BucketGeo g = bucket_geo(L, n, m, h->num_sms);
   const int64_t tot = n + m;
+  const int64_t nfcap = final_buckets_cap(g, kLcCap);
   Carver c;
   const size_t o_sst = c.take<uint64_t>(ceil_div(g.nb, kScanBuckets));
-  const size_t o_lst = c.take<uint64_t>(g.nb);
-  const size_t o_ctl = c.take<uint32_t>(4);  // [0] scan ticket, [1] local ticket, [2] max bucket
+  const size_t o_pst = c.take<uint64_t>(ceil_div(g.nb, 256));
+  const size_t o_lst = c.take<uint64_t>(nfcap);
+  const size_t o_ctl = c.take<uint32_t>(8);  // [0] scan ticket, [1] plan ticket, [2] max bucket, [3] nfinal
+  const size_t o_fine = c.take<uint32_t>((int64_t)g.nb * kRefBins);
+  const size_t o_gtab = c.take<uint8_t>((int64_t)g.nb * kRefBins);
   const size_t zero_bytes = c.off;
   const size_t o_mat = c.take<uint32_t>((int64_t)g.hgrid * g.nb);
   const size_t o_bs = c.take<uint32_t>(g.nb + 1);
-  const size_t o_cur = c.take<uint32_t>((int64_t)g.nb * kCursorStride);
+  const size_t o_fb = c.take<uint32_t>(g.nb);
+  const size_t o_bsf = c.take<uint32_t>(nfcap + 1);
+  const size_t o_desc = c.take<BDesc>(nfcap);
+  const size_t o_cur = c.take<uint32_t>(nfcap * kCursorStride);
   const size_t o_rec = c.take<double>(4 * tot);
   const size_t o_idx = c.take<uint32_t>(tot);
   char* w = nullptr;
@@ -232,19 +249,32 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
   uint32_t* ctl = (uint32_t*)(w + o_ctl);
   uint32_t* mat = (uint32_t*)(w + o_mat);
   uint32_t* bstart = (uint32_t*)(w + o_bs);
-  uint32_t* cursor = (uint32_t*)(w + o_cur);
   double* rec = (double*)(w + o_rec);
   uint32_t* idx = (uint32_t*)(w + o_idx);
   uint64_t* sst = (uint64_t*)(w + o_sst);
   uint64_t* lst = (uint64_t*)(w + o_lst);
+  PlanOut po{};
+  po.fbase = (uint32_t*)(w + o_fb);
+  po.gtab = (uint8_t*)(w + o_gtab);
+  po.bstart_f = (uint32_t*)(w + o_bsf);
+  po.desc = (BDesc*)(w + o_desc);
+  po.cursor = (uint32_t*)(w + o_cur);
+  po.nfinal = ctl + 3;
+  po.fail = &dplan->fail;
+  po.states = (uint64_t*)(w + o_pst);
+  po.ticket = ctl + 1;
+  uint32_t* fine = (uint32_t*)(w + o_fine);
   const bool narrow = L <= 10;
   if (narrow)
-    launch_hs<true>(src, q, recv, g, h->num_sms, L, mat, bstart, cursor, sst, ctl, rec, idx, &dplan->err, s);
+    launch_hs<true>(src, q, recv, g, h->num_sms, L, mat, bstart, sst, ctl, fine, po, rec, idx,
+                    &dplan->err, s);
   else
-    launch_hs<false>(src, q, recv, g, h->num_sms, L, mat, bstart, cursor, sst, ctl, rec, idx, &dplan->err, s);
+    launch_hs<false>(src, q, recv, g, h->num_sms, L, mat, bstart, sst, ctl, fine, po, rec, idx,
+                     &dplan->err, s);
   const bool ck32 = g.shift + g.cbits <= 32;
-#define FMMB_LOCAL(CK, NW, HD) \
-  launch_local<CK, NW, HD>(rec, idx, bstart, g, L, o, lst, ctl, &dplan->fail, s)
+#define FMMB_LOCAL(CK, NW, HD)                                                               \
+  launch_local<CK, NW, HD>(h, rec, idx, po.bstart_f, po.desc, po.nfinal, g, L, o, lst, po.fail, \
+                           s)
   if (heads) {
     if (narrow) { if (ck32) FMMB_LOCAL(uint32_t, true, true); else FMMB_LOCAL(uint64_t, true, true); }
     else { if (ck32) FMMB_LOCAL(uint32_t, false, true); else FMMB_LOCAL(uint64_t, false, true); }
@@ -253,10 +283,12 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
     else { if (ck32) FMMB_LOCAL(uint32_t, false, false); else FMMB_LOCAL(uint64_t, false, false); }
   }
 #undef FMMB_LOCAL
-  launches += 4;
+  launches += 6;
   run.scratch = w;
   run.g = g;
-  run.bstart = bstart;
+  run.bstart_f = po.bstart_f;
+  run.desc = po.desc;
+  run.nfinal = po.nfinal;
   run.hpos = idx;
   return FMMB_OK;
 }
@@ -495,12 +527,13 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
         }
         hpar.ktot_src = dplan->ktot + L;
         hpar.ktot_recv = dplan->ktot + stride + L;
-        hpar.bstart = brun.bstart;
+        hpar.bstart = brun.bstart_f;
         hpar.hpos = brun.hpos;
         hpar.ne = ne_out;
         hpar.bm = bm_out;
         hpar.kinfo = dplan->kinfo;
-        k_bkt_heads<<<(unsigned)ceil_div(brun.g.nb, 8), 256, 0, s>>>(hpar, brun.g);
+        k_bkt_heads<<<(unsigned)h->num_sms * 8, 256, 0, s>>>(hpar, brun.desc, brun.nfinal,
+                                                              brun.g);
         ++launches;
       }
       cudaFreeAsync(brun.scratch, s);

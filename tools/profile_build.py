@@ -12,6 +12,6 @@ st = fb.build_all_device(src, q, recv, wl.level); st = None
 torch.cuda.synchronize()
 for _ in range(reps):
     st = fb.build_all_device(src, q, recv, wl.level)
-    print({k: round(v * 1e3, 3) for k, v in st.build_seconds.items()}, st.n_launches)
+    print({k: round(v * 1e3, 3) for k, v in st.build_seconds.items()}, st.n_launches, st.sort_path)
     st = None
 torch.cuda.synchronize()
