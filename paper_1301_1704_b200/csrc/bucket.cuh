@@ -644,6 +644,21 @@ __device__ __forceinline__ void lc_pass(const CK* kin, const uint16_t* pin, CK* 
   __syncthreads();
 }
 
+// One 24-byte point row with two stores: the 16-byte-aligned pair as one
+// 16-byte store (x,y for an even row, y,z for an odd one) plus the other
+// coordinate, instead of three 8-byte stores per row.
+__device__ __forceinline__ void store_row(double* pts, int64_t p, double x, double y, double z) {
+  // (explicit PTX: the two branch-wise equivalent forms must not be merged into
+  // one unaligned 16-byte store)
+  const bool odd = p & 1;
+  double* row = pts + 3 * p;
+  double* pair = row + (odd ? 1 : 0);
+  double* one = row + (odd ? 0 : 2);
+  asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(pair), "d"(odd ? y : x), "d"(odd ? z : y)
+               : "memory");
+  asm volatile("st.global.f64 [%0], %1;" ::"l"(one), "d"(odd ? x : z) : "memory");
+}
+
 struct LocalOut {
   double* pts;
   double* q;
@@ -695,16 +710,18 @@ __global__ void __launch_bounds__(kLcThreads)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   if (__ldg(fail)) return;  // a final bucket overflows: the host reruns on the general path
   uint64_t* bar = s_misc + 2;
+  const uint32_t nf = __ldg(nfinal);
   if (tid == 0) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(bar)));
+    mbar_init(bar);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const uint32_t nf = __ldg(nfinal);
   uint32_t bar_phase = 0;
   const int64_t n = g.n, m = g.m, tot = n + m;
   // persistent: every resident CTA walks the final buckets round-robin (in
-  // order, so the non-HEADS look-back always finds its predecessors running)
+  // order, so the non-HEADS look-back always finds its predecessors running).
+  // (Double-buffering the records to prefetch the next bucket costs the third
+  // resident CTA per SM and measured slower: 0.86 vs 0.69 ms at c2.)
   for (int64_t tile = blockIdx.x; tile < nf; tile += gridDim.x) {
   const int64_t bs = bstart[tile];
   const int B = (int)(bstart[tile + 1] - bs);
@@ -726,24 +743,16 @@ __global__ void __launch_bounds__(kLcThreads)
   }
 
   // phase 0: bulk copy of the bucket's records (TMA), source indices by LDG
-  if (tid == 0 && B > 0) {
+  if (tid == 0) {
     const uint32_t bytes = (uint32_t)B * 32u;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-    asm volatile(
-        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::
-            "r"(smem_u32(s_rec)),
-        "l"(rec + 4 * (size_t)bs), "r"(bytes), "r"(smem_u32(bar))
-        : "memory");
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(s_rec, rec + 4 * (size_t)bs, bytes, bar);
   }
   if (set == 0)
     for (int j = tid; j < B; j += kLcThreads) s_idx[j] = __ldg(idx + bs + j);
-  if (B > 0) {
-    mbar_wait(bar, bar_phase);
-    bar_phase ^= 1u;
-  }
+  mbar_wait(bar, bar_phase);
+  bar_phase ^= 1u;
   __syncthreads();
   // phase 1: low key bits and combined input index of every record; with
   // HEADS and <= 2^12 boxes per bucket also the per-box counts
@@ -757,7 +766,10 @@ __global__ void __launch_bounds__(kLcThreads)
     const double* r = s_rec + 4 * j;
     const uint64_t key = encode_any<NARROW>(r[0], r[1], r[2], level, grid);
     const uint32_t ci = set == 0 ? s_idx[j] : (uint32_t)(n + __double_as_longlong(r[3]));
-    const uint64_t lk = key - prefix;  // < span
+    // < span for every valid point; out-of-grid inputs (reported as a DomainError
+    // after the build) are clamped so they cannot index outside the bucket
+    uint64_t lk = (key & ((1ull << g.sbits) - 1ull)) - prefix;
+    if (lk >= span) lk = 0;
     if (small) {
       k0[j] = (CK)lk;
       s_idx[j] = ci;
@@ -849,10 +861,7 @@ __global__ void __launch_bounds__(kLcThreads)
       const int64_t p = bs + pos;
       const int j = p0[pos];
       const double* r = s_rec + 4 * j;
-      double* po = o.pts + 3 * p;
-      po[0] = r[0];
-      po[1] = r[1];
-      po[2] = r[2];
+      store_row(o.pts, p, r[0], r[1], r[2]);
       if (set == 0) {
         if (o.q) o.q[p] = r[3];
         o.perm[p] = perm_of(o, 0, (int64_t)s_idx[j]);
@@ -933,10 +942,7 @@ __global__ void __launch_bounds__(kLcThreads)
       const int pl = pc[j];
       const double* r = s_rec + 4 * pl;
       const uint64_t mk = prefix + lk;
-      double* po = o.pts + 3 * p;
-      po[0] = r[0];
-      po[1] = r[1];
-      po[2] = r[2];
+      store_row(o.pts, p, r[0], r[1], r[2]);
       if (set == 0) {
         if (o.q) o.q[p] = r[3];
         o.perm[p] = perm_of(o, 0, (int64_t)s_idx[pl]);
