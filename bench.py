@@ -261,6 +261,14 @@ def run_ours(args):
           for k in ("sort_sources", "level_directory", "lists_count", "size_readback",
                     "lists_write")}
     peak, peak_src = roofline.measured_hbm_gbs(ROOT)
+    traffic = None  # DRAM bytes per launch of the dominant kernel, from the committed ncu capture
+    try:
+        with open(os.path.join(ROOT, "profiles", "roofline_traffic.json")) as f:
+            t = json.load(f).get("k_lists_write", {})
+        if t.get("workload") == args.workload:
+            traffic = int(t["dram_bytes_per_launch"])
+    except (OSError, ValueError, KeyError):
+        pass
     write_s = ph["lists_write"] * 1e-3
     achieved = wbytes / write_s / 1e9
     build_gbs = balg / (elapsed / args.steps) / 1e9
@@ -306,7 +314,7 @@ def run_ours(args):
             "roofline": {
                 "bound": "hbm", "kernel": "k_lists_write (E2+E4 list write)",
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "peak_source": peak_src, "traffic": None,
+                "peak_source": peak_src, "traffic": traffic,
                 "alg_bytes_per_launch": wbytes, "avg_launch_ms": ph["lists_write"],
             },
             "build_roofline": {
