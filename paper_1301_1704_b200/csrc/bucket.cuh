@@ -375,6 +375,38 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// ------------------------------------------------ speculative regions ----
+// Uniform inputs skip the histogram pass: every coarse bucket gets a region of
+// kLcCap record slots (the local sort's capacity), the scatter claims slots
+// from region cursors, and the exact output starts come from the final
+// cursors afterwards.  A region overflow (a skewed input) raises spec_fail
+// and the host reruns the sort phase with the histogram pass.  Regions are
+// kSpecStride (odd) records apart, so the 2^15 region fronts do not all fall
+// on the same DRAM / L2 address bits.
+constexpr int kSpecStride = 1281;
+__global__ void __launch_bounds__(256)
+    k_spec_init(const BucketGeo g, uint32_t cap, uint32_t* __restrict__ cursor,
+                uint32_t* __restrict__ rbase, BDesc* __restrict__ desc,
+                uint32_t* __restrict__ nfinal) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b == 0) *nfinal = (uint32_t)g.nb;
+  if (b >= g.nb) return;
+  cursor[(size_t)b * kCursorStride] = (uint32_t)b * cap;
+  rbase[b] = (uint32_t)b * cap;
+  const uint64_t set = (uint64_t)(b >> g.bb);
+  desc[b] = BDesc{(uint64_t)(b & ((1 << g.bb) - 1)) << g.shift, (1ull << g.shift) | (set << 63)};
+}
+
+// region fill counts, in the layout k_bkt_scan sums (one histogram row)
+__global__ void __launch_bounds__(256)
+    k_spec_counts(const BucketGeo g, uint32_t cap, const uint32_t* __restrict__ cursor,
+                  uint32_t* __restrict__ counts) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= g.nb) return;
+  const uint32_t c = cursor[(size_t)b * kCursorStride] - (uint32_t)b * cap;
+  counts[b] = c < cap ? c : cap;
+}
+
 // ---------------------------------------------------------- scatter pass --
 __device__ __forceinline__ void st_v4f64(double* p, double a, double b, double c, double d) {
   asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(p), "d"(a), "d"(b), "d"(c),
@@ -447,6 +479,9 @@ struct FinalMap {  // coarse bucket (+ next kRefBits key bits) -> final bucket
   const uint8_t* gtab;
   const uint32_t* maxb;
   uint32_t cap;
+  uint32_t spec_cap;   // speculative regions: spec_cap slots apart, `cap` usable (0: exact starts)
+  uint32_t* spec_fail; // raised when a region overflows
+  uint32_t* err;       // speculative mode: out-of-grid keys (the skipped histogram pass checks them)
 };
 
 template <bool NARROW>
@@ -524,18 +559,25 @@ __global__ void __launch_bounds__(kSThreads, 1)
       xyz[3 * tid + 2] = __ldg(p + 2);
       if (i < n) xyz[3 * kSRows + tid] = q ? __ldg(q + i) : 0.0;
     }
-    const uint64_t key =
-        encode_any<NARROW>(xyz[3 * tid], xyz[3 * tid + 1], xyz[3 * tid + 2], level, grid) & kmask;
+    const uint64_t raw =
+        encode_any<NARROW>(xyz[3 * tid], xyz[3 * tid + 1], xyz[3 * tid + 2], level, grid);
+    if (fm.err && raw > kmask) atomicOr(fm.err, 1u);
+    const uint64_t key = raw & kmask;
     uint32_t b = bucket_of(key, i >= n, g);
     if (refined)
       b = __ldg(fm.fbase + b) +
           __ldg(fm.gtab + (size_t)b * kRefBins + ((key >> (g.shift - R)) & ((1u << R) - 1u)));
-    return atomicAdd(cursor + (size_t)b * kCursorStride, 1u);
+    const uint32_t slot = atomicAdd(cursor + (size_t)b * kCursorStride, 1u);
+    if (fm.spec_cap && slot - b * fm.spec_cap >= fm.cap) {  // region full
+      atomicOr(fm.spec_fail, 1u);
+      return 0xFFFFFFFFu;
+    }
+    return slot;
   };
   auto store = [&](int k, uint32_t dst) {
     const double* xyz = stage_xyz(k);
     const int64_t i = lo + (int64_t)k * kSRows + tid;
-    if (tid < stage_rows(k)) {
+    if (tid < stage_rows(k) && dst != 0xFFFFFFFFu) {
       const double w = i < n ? (q ? xyz[3 * kSRows + tid] : 0.0) : __longlong_as_double(i - n);
       st_v4f64(rec + 4 * (size_t)dst, xyz[3 * tid], xyz[3 * tid + 1], xyz[3 * tid + 2], w);
       if (i < n) idx[dst] = (uint32_t)i;
@@ -692,9 +734,9 @@ __device__ __forceinline__ int64_t perm_of(const LocalOut& o, int set, int64_t l
 template <typename CK, bool NARROW, bool HEADS>
 __global__ void __launch_bounds__(kLcThreads)
     k_bkt_local(const double* __restrict__ rec, uint32_t* __restrict__ idx,
-                const uint32_t* __restrict__ bstart, const BDesc* __restrict__ desc,
-                const uint32_t* __restrict__ nfinal, const BucketGeo g, int level,
-                const LocalOut o, uint64_t* __restrict__ states,
+                const uint32_t* __restrict__ bstart, const uint32_t* __restrict__ rbase,
+                const BDesc* __restrict__ desc, const uint32_t* __restrict__ nfinal,
+                const BucketGeo g, int level, const LocalOut o, uint64_t* __restrict__ states,
                 const uint32_t* __restrict__ fail) {
   extern __shared__ __align__(128) unsigned char lc_smem[];
   double* s_rec = reinterpret_cast<double*>(lc_smem);                   // [cap][4]
@@ -723,8 +765,9 @@ __global__ void __launch_bounds__(kLcThreads)
   // (Double-buffering the records to prefetch the next bucket costs the third
   // resident CTA per SM and measured slower: 0.86 vs 0.69 ms at c2.)
   for (int64_t tile = blockIdx.x; tile < nf; tile += gridDim.x) {
-  const int64_t bs = bstart[tile];
+  const int64_t bs = bstart[tile];  // output position of the bucket's first point
   const int B = (int)(bstart[tile + 1] - bs);
+  const int64_t rb = rbase ? (int64_t)rbase[tile] : bs;  // its first record (speculative regions)
   const BDesc d = desc[tile];
   const int set = (int)(d.span_set >> 63);
   const uint64_t span = d.span_set & ~(1ull << 63);
@@ -747,10 +790,10 @@ __global__ void __launch_bounds__(kLcThreads)
     const uint32_t bytes = (uint32_t)B * 32u;
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic reads
     mbar_expect_tx(bar, bytes);
-    bulk_g2s(s_rec, rec + 4 * (size_t)bs, bytes, bar);
+    bulk_g2s(s_rec, rec + 4 * (size_t)rb, bytes, bar);
   }
   if (set == 0)
-    for (int j = tid; j < B; j += kLcThreads) s_idx[j] = __ldg(idx + bs + j);
+    for (int j = tid; j < B; j += kLcThreads) s_idx[j] = __ldg(idx + rb + j);
   mbar_wait(bar, bar_phase);
   bar_phase ^= 1u;
   __syncthreads();
@@ -812,7 +855,7 @@ __global__ void __launch_bounds__(kLcThreads)
     ranked = mx <= 64;
     uint32_t start = x & 0xFFFFu, hidx = x >> 16;
     unsigned long long* bm = set ? o.bmp[1] : o.bmp[0];
-    uint32_t* hp = idx + bs;
+    uint32_t* hp = idx + rb;
 #pragma unroll
     for (int e = 0; e < kBpt; ++e) {
       const int i = tid * kBpt + e;
@@ -915,7 +958,7 @@ __global__ void __launch_bounds__(kLcThreads)
     hbase = (int64_t)s_misc[1];
   }
   unsigned long long* bmp = set ? o.bmp[1] : o.bmp[0];
-  uint32_t* hpos = idx + bs;  // HEADS: this bucket's idx slots are free again
+  uint32_t* hpos = idx + rb;  // HEADS: this bucket's idx slots are free again
   const unsigned lt = lanemask_lt();
   // phase 4: outputs in sorted order (chunks of kLcThreads, scan of heads)
   for (int j0 = 0; j0 < B; j0 += kLcThreads) {
@@ -993,6 +1036,7 @@ struct HeadsParams {
   const int64_t* ktot_src;  // K_s (device, from k_rank)
   const int64_t* ktot_recv; // K_r
   const uint32_t* bstart;
+  const uint32_t* rbase;  // record / hpos base per final bucket (null: = bstart)
   const uint32_t* hpos;
   uint64_t* ne;
   int64_t* bm;
@@ -1022,7 +1066,7 @@ __global__ void __launch_bounds__(256)
     const uint64_t key0 = d.lo;
     const uint64_t* bmp = set ? hp.bmp[1] : hp.bmp[0];
     const uint32_t* dir = set ? hp.dir[1] : hp.dir[0];
-    const uint32_t* hpos = hp.hpos + hp.bstart[f];
+    const uint32_t* hpos = hp.hpos + (hp.rbase ? hp.rbase[f] : hp.bstart[f]);
     uint64_t* ne = hp.ne + (set ? ks : 0);
     int64_t* bm = hp.bm + (set ? ks + 1 : 0);
     const int64_t w0 = (int64_t)(key0 >> 6);

@@ -177,7 +177,8 @@ struct BuildPlanHost {  // mirrored in the pinned readback block
   int64_t seg_totals[kMaxLevel + 1];
   int64_t kinfo[2];
   uint32_t err;
-  uint32_t fail;  // bucket path overflowed its shared-memory capacity
+  uint32_t fail;       // bucket path overflowed its shared-memory capacity
+  uint32_t spec_fail;  // a speculative bucket region overflowed
 };
 
 // ---- sort phase, fast path: payload-carrying bucket sort (bucket.cuh)
@@ -185,6 +186,7 @@ struct BucketRun {  // scratch that outlives the sort phase (heads pass)
   char* scratch = nullptr;
   BucketGeo g{};
   const uint32_t* bstart_f = nullptr;
+  const uint32_t* rbase = nullptr;
   const BDesc* desc = nullptr;
   const uint32_t* nfinal = nullptr;
   const uint32_t* hpos = nullptr;
@@ -192,14 +194,33 @@ struct BucketRun {  // scratch that outlives the sort phase (heads pass)
 
 template <typename CK, bool NARROW, bool HEADS>
 void launch_local(fmmb_handle_t h, const double* rec, uint32_t* idx, const uint32_t* bstart_f,
-                  const BDesc* desc, const uint32_t* nfinal, const BucketGeo& g, int L,
-                  const LocalOut& o, uint64_t* lst, const uint32_t* fail, cudaStream_t s) {
+                  const uint32_t* rbase, const BDesc* desc, const uint32_t* nfinal,
+                  const BucketGeo& g, int L, const LocalOut& o, uint64_t* lst,
+                  const uint32_t* fail, cudaStream_t s) {
   auto kern = k_bkt_local<CK, NARROW, HEADS>;
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLcThreads, lc_smem_bytes<CK>());
   const int grid = std::max(1, per_sm) * h->num_sms;  // persistent: all CTAs resident
-  kern<<<grid, kLcThreads, lc_smem_bytes<CK>(), s>>>(rec, idx, bstart_f, desc, nfinal, g, L, o,
-                                                     lst, fail);
+  kern<<<grid, kLcThreads, lc_smem_bytes<CK>(), s>>>(rec, idx, bstart_f, rbase, desc, nfinal, g,
+                                                     L, o, lst, fail);
+}
+
+template <bool NARROW>
+void launch_spec(const double* src, const double* q, const double* recv, const BucketGeo& g,
+                 int num_sms, int L, uint32_t* counts, uint32_t* bstart, uint64_t* sst,
+                 uint32_t* ctl, uint32_t* rbase, const PlanOut& po, double* rec, uint32_t* idx,
+                 uint32_t* spec_fail, uint32_t* err, cudaStream_t s) {
+  const unsigned nbg = (unsigned)ceil_div(g.nb, 256);
+  k_spec_init<<<nbg, 256, 0, s>>>(g, kSpecStride, po.cursor, rbase, po.desc, po.nfinal);
+  const int sgrid = (int)std::min<int64_t>(num_sms, ceil_div(g.n + g.m, kSRows));
+  const FinalMap fm{po.fbase, po.gtab, ctl + 4, kLcCap, (uint32_t)kSpecStride, spec_fail, err};
+  k_bkt_scatter<NARROW><<<(unsigned)sgrid, kSThreads, scatter_smem_bytes(), s>>>(
+      src, q, recv, g, L, scatter_rows_per_cta(g.n + g.m, sgrid), po.cursor, rec, idx, fm);
+  k_spec_counts<<<nbg, 256, 0, s>>>(g, kSpecStride, po.cursor, counts);
+  BucketGeo g1 = g;
+  g1.hgrid = 1;
+  k_bkt_scan<<<(unsigned)ceil_div(g.nb, kScanBuckets), 256, 0, s>>>(counts, g1, bstart, sst,
+                                                                    ctl + 0, ctl + 2);
 }
 
 template <bool NARROW>
@@ -214,23 +235,27 @@ void launch_hs(const double* src, const double* q, const double* recv, const Buc
   k_bkt_fine<NARROW><<<num_sms * 8, 256, 0, s>>>(src, recv, g, L, bstart, ctl + 2, kLcCap, fine);
   k_bkt_plan<<<(unsigned)ceil_div(g.nb, 256), 256, 0, s>>>(g, bstart, ctl + 2, kLcCap, fine, po);
   const int sgrid = (int)std::min<int64_t>(num_sms, ceil_div(g.n + g.m, kSRows));
-  const FinalMap fm{po.fbase, po.gtab, ctl + 2, kLcCap};
+  const FinalMap fm{po.fbase, po.gtab, ctl + 2, kLcCap, 0u, nullptr, nullptr};
   k_bkt_scatter<NARROW><<<(unsigned)sgrid, kSThreads, scatter_smem_bytes(), s>>>(
       src, q, recv, g, L, scatter_rows_per_cta(g.n + g.m, sgrid), po.cursor, rec, idx, fm);
 }
 
+// speculative regions apply when the coarse buckets already fit the count path
+inline bool spec_possible(const BucketGeo& g) { return g.shift <= kLcSmallBits; }
+
 fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int64_t n,
                         const double* recv, int64_t m, int L, const LocalOut& o, bool heads,
-                        BuildPlanHost* dplan, cudaStream_t s, int64_t& launches,
+                        bool spec, BuildPlanHost* dplan, cudaStream_t s, int64_t& launches,
                         BucketRun& run) {
   const BucketGeo g = bucket_geo(L, n, m, h->num_sms);
   const int64_t tot = n + m;
   const int64_t nfcap = final_buckets_cap(g, kLcCap);
+  const int64_t nrec = spec ? (int64_t)g.nb * kSpecStride : tot;  // record slots
   Carver c;
   const size_t o_sst = c.take<uint64_t>(ceil_div(g.nb, kScanBuckets));
   const size_t o_pst = c.take<uint64_t>(ceil_div(g.nb, 256));
   const size_t o_lst = c.take<uint64_t>(nfcap);
-  const size_t o_ctl = c.take<uint32_t>(8);  // [0] scan ticket, [1] plan ticket, [2] max bucket, [3] nfinal
+  const size_t o_ctl = c.take<uint32_t>(8);  // [0] scan ticket, [1] plan ticket, [2] max bucket, [3] nfinal, [4] zero
   const size_t o_fine = c.take<uint32_t>((int64_t)g.nb * kRefBins);
   const size_t o_gtab = c.take<uint8_t>((int64_t)g.nb * kRefBins);
   const size_t zero_bytes = c.off;
@@ -240,8 +265,9 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
   const size_t o_bsf = c.take<uint32_t>(nfcap + 1);
   const size_t o_desc = c.take<BDesc>(nfcap);
   const size_t o_cur = c.take<uint32_t>(nfcap * kCursorStride);
-  const size_t o_rec = c.take<double>(4 * tot);
-  const size_t o_idx = c.take<uint32_t>(tot);
+  const size_t o_rec = c.take<double>(4 * nrec);
+  const size_t o_idx = c.take<uint32_t>(nrec);
+  const size_t o_rb = c.take<uint32_t>(spec ? g.nb : 0);
   char* w = nullptr;
   if (cudaMallocAsync((void**)&w, c.off, s) != cudaSuccess)
     return fmmb_fail(h, FMMB_ERR_CUDA, "bucket-sort scratch of %zu bytes failed", c.off);
@@ -265,16 +291,27 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
   po.ticket = ctl + 1;
   uint32_t* fine = (uint32_t*)(w + o_fine);
   const bool narrow = L <= 10;
-  if (narrow)
+  uint32_t* rbase = spec ? (uint32_t*)(w + o_rb) : nullptr;
+  if (spec) {  // no histogram pass: fixed regions, exact starts from the final cursors
+    if (narrow)
+      launch_spec<true>(src, q, recv, g, h->num_sms, L, mat, bstart, sst, ctl, rbase, po, rec,
+                        idx, &dplan->spec_fail, &dplan->err, s);
+    else
+      launch_spec<false>(src, q, recv, g, h->num_sms, L, mat, bstart, sst, ctl, rbase, po, rec,
+                         idx, &dplan->spec_fail, &dplan->err, s);
+    po.bstart_f = bstart;
+  } else if (narrow) {
     launch_hs<true>(src, q, recv, g, h->num_sms, L, mat, bstart, sst, ctl, fine, po, rec, idx,
                     &dplan->err, s);
-  else
+  } else {
     launch_hs<false>(src, q, recv, g, h->num_sms, L, mat, bstart, sst, ctl, fine, po, rec, idx,
                      &dplan->err, s);
+  }
+  const uint32_t* lfail = spec ? &dplan->spec_fail : po.fail;
   const bool ck32 = g.shift + g.cbits <= 32;
-#define FMMB_LOCAL(CK, NW, HD)                                                               \
-  launch_local<CK, NW, HD>(h, rec, idx, po.bstart_f, po.desc, po.nfinal, g, L, o, lst, po.fail, \
-                           s)
+#define FMMB_LOCAL(CK, NW, HD)                                                             \
+  launch_local<CK, NW, HD>(h, rec, idx, po.bstart_f, rbase, po.desc, po.nfinal, g, L, o, lst, \
+                           lfail, s)
   if (heads) {
     if (narrow) { if (ck32) FMMB_LOCAL(uint32_t, true, true); else FMMB_LOCAL(uint64_t, true, true); }
     else { if (ck32) FMMB_LOCAL(uint32_t, false, true); else FMMB_LOCAL(uint64_t, false, true); }
@@ -287,6 +324,7 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
   run.scratch = w;
   run.g = g;
   run.bstart_f = po.bstart_f;
+  run.rbase = rbase;
   run.desc = po.desc;
   run.nfinal = po.nfinal;
   run.hpos = idx;
@@ -454,6 +492,9 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
 
   int64_t launches = 0;
   bool fast = h->sort_path != 2 && tot > 0;
+  // speculative bucket regions (no histogram pass) unless this shape missed last time
+  bool spec = fast && spec_possible(bucket_geo(L, n, m, h->num_sms)) &&
+              !(h->spec_miss_level == L && h->spec_miss_n == n && h->spec_miss_m == m);
   BuildPlanHost* hp = (BuildPlanHost*)h->pinned;
   ListsParams lp{};
   int64_t nwork_cap = 0;
@@ -467,7 +508,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     BucketRun brun;
     if (tot > 0) {
       const fmmb_status st =
-          fast ? sort_bucket(h, src, q, n, recv, m, L, lo, lists, dplan, s, launches, brun)
+          fast ? sort_bucket(h, src, q, n, recv, m, L, lo, lists, spec, dplan, s, launches, brun)
                : sort_onesweep<KeyT>(h, src, q, n, recv, m, L, lo, dplan, s, launches);
       if (st != FMMB_OK) {
         cudaFreeAsync(ws, s);
@@ -528,6 +569,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
         hpar.ktot_src = dplan->ktot + L;
         hpar.ktot_recv = dplan->ktot + stride + L;
         hpar.bstart = brun.bstart_f;
+        hpar.rbase = brun.rbase;
         hpar.hpos = brun.hpos;
         hpar.ne = ne_out;
         hpar.bm = bm_out;
@@ -572,8 +614,16 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
       cudaFreeAsync(ws, s);
       return fmmb_fail(h, FMMB_ERR_CUDA, "build phase A failed: %s", cudaGetErrorString(ce));
     }
-    if (hp->fail && fast && attempt == 0) {  // a bucket overflowed: general sort
+    if (spec && hp->spec_fail && attempt < 2) {  // a speculative region overflowed
+      h->spec_miss_level = L;
+      h->spec_miss_n = n;
+      h->spec_miss_m = m;
+      spec = false;
+      continue;
+    }
+    if (hp->fail && fast && attempt < 2) {  // a bucket overflowed: general sort
       fast = false;
+      spec = false;
       continue;
     }
     break;

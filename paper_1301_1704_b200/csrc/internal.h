@@ -13,6 +13,9 @@ struct fmmb_handle_s {
   int64_t launches = 0;
   int sort_path = 0;       // 0 auto (bucket sort, Onesweep on overflow), 1 bucket, 2 Onesweep
   int last_sort_path = 0;  // path the last build's sort phase completed on
+  // geometry (level, n, m) whose speculative bucket regions last overflowed:
+  // the next build of the same shape starts with the histogram pass
+  int64_t spec_miss_level = -1, spec_miss_n = -1, spec_miss_m = -1;
   std::string err;
 };
 

@@ -77,6 +77,22 @@ def test_crowded_box_inside_bucket(gpu, ref):
     assert not compare_structures(got, want)
 
 
+def test_overfull_bucket_is_refined(gpu, ref):
+    """A coarse bucket with 3x the shared-memory capacity: the speculative
+    regions overflow, the histogram pass refines the bucket into sub-bin
+    groups, and the build stays on the bucket path (twice: the second build
+    of the same shape starts with the histogram pass)."""
+    src, q, recv = generate(2**16, 2**16, "uniform", 41)
+    extra = np.random.default_rng(2).random((3000, 3)) * 0.25  # one level-2 box
+    src = np.concatenate([src, extra])
+    q = np.concatenate([q, np.ones(3000)])
+    want = ref.build_all(src, q, recv, max_level=5)
+    for _ in range(2):
+        got = gpu.build_all(src, q, recv, max_level=5)
+        assert got.sort_path == "bucket"
+        assert not compare_structures(got, want)
+
+
 def test_uniform_build_takes_bucket_path(gpu, ref):
     src, q, recv = generate(2**17, 2**17, "uniform", 21)
     want = ref.build_all(src, q, recv, max_level=6)
