@@ -52,6 +52,8 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--sort-path", default="auto",
+                   choices=["auto", "bucket", "onesweep", "bucket_hist"])
     return p.parse_args()
 
 
@@ -197,6 +199,7 @@ def run_ours(args):
     else:
         torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
+    fb._lib.set_sort_path(args.sort_path, dev)
     wl = WORKLOADS[args.workload]
     src_np, q_np, recv_np = generate(wl.n, wl.n, wl.dist, wl.seed + rank)
     src = torch.from_numpy(src_np).to(dev)

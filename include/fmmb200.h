@@ -72,7 +72,8 @@ FMMB_API int64_t fmmb_last_launch_count(fmmb_handle_t h);
  * counterpart; both strategies give bit-identical outputs):
  *   0 = auto: payload-carrying bucket sort, rerun on the Onesweep path if a
  *       bucket overflows the bucket sort's shared-memory capacity;
- *   1 = bucket sort (with the same overflow rerun);  2 = Onesweep LSD + gather.
+ *   1 = bucket sort (with the same overflow rerun);  2 = Onesweep LSD + gather;
+ *   3 = bucket sort without speculative fixed regions (histogram pass first).
  * fmmb_last_sort_path() reports the path the last build completed on (1/2). */
 FMMB_API fmmb_status fmmb_set_sort_path(fmmb_handle_t h, int path);
 FMMB_API int fmmb_last_sort_path(fmmb_handle_t h);
@@ -253,6 +254,37 @@ FMMB_API fmmb_status fmmb_dist_sort(fmmb_handle_t h, const double* src, const do
 FMMB_API fmmb_status fmmb_dist_lists(fmmb_handle_t h, const uint64_t* gbmp, int level,
                             uint64_t key_lo, uint64_t key_hi, fmmb_alloc_fn alloc, void* ctx,
                             fmmb_structures* out, void* stream);
+
+/* ------------------------------------------- consumers of the structures */
+
+/* near_field(sx, sy, sz, sq, src_bookmark, nbr_bookmark, nbr_list, rx, ry,
+ * rz, recv_bookmark) (_ckernels.pyx:290-323; caller fmm.py:173-190):
+ * phi[r] for every receiver r of receiver box j = sum over the sources of
+ * the boxes nbr_list[nbr_bookmark[j]:nbr_bookmark[j+1]] (segment order,
+ * points in sorted order) of q/|r - s|, skipping coincident pairs.
+ * Bit-identical to the compiled backend (sequential f64 sum, IEEE sqrt and
+ * divide, no contraction).  Coordinates strided by *_stride ELEMENTS; q may
+ * be NULL (unit charges).  Receivers outside every box get 0.
+ * nbr_bookmark and recv_bookmark both have n_recv_boxes + 1 entries. */
+FMMB_API fmmb_status fmmb_near_field(fmmb_handle_t h, const double* sx, int64_t sx_stride,
+                            const double* sy, int64_t sy_stride, const double* sz,
+                            int64_t sz_stride, const double* q, int64_t ns,
+                            const int64_t* src_bookmark, int64_t n_src_boxes,
+                            const int64_t* nbr_bookmark, const int64_t* nbr_list,
+                            int64_t n_nbr, const double* rx, int64_t rx_stride,
+                            const double* ry, int64_t ry_stride, const double* rz,
+                            int64_t rz_stride, int64_t nr, const int64_t* recv_bookmark,
+                            int64_t n_recv_boxes, double* phi, void* stream);
+
+/* direct_potentials(sx, sy, sz, sq, rx, ry, rz) (_ckernels.pyx:326-350;
+ * caller fmm.py:21-30 direct_sum): every receiver against every source in
+ * source order, same exactness contract as fmmb_near_field. */
+FMMB_API fmmb_status fmmb_direct_potentials(fmmb_handle_t h, const double* sx,
+                                   int64_t sx_stride, const double* sy, int64_t sy_stride,
+                                   const double* sz, int64_t sz_stride, const double* q,
+                                   int64_t ns, const double* rx, int64_t rx_stride,
+                                   const double* ry, int64_t ry_stride, const double* rz,
+                                   int64_t rz_stride, int64_t nr, double* phi, void* stream);
 
 #ifdef __cplusplus
 }

@@ -42,6 +42,8 @@ def load():
         lib.orc_stencil_segments.argtypes = [p, i64, p, i64, C.c_int, p, p, p]
         lib.orc_stencil_segments.restype = i64
         lib.orc_propagate.argtypes = [p, i64, p]
+        lib.orc_near_field.argtypes = [p, p, p, p, p, p, p, i64, i64, p]
+        lib.orc_direct.argtypes = [p, p, i64, p, i64, p]
         lib.orc_propagate.restype = i64
         _lib = lib
     return _lib
@@ -149,3 +151,27 @@ def build_all(src, charges, recv, level: int) -> SimpleNamespace:
         directory=SimpleNamespace(max_level=level, src_boxes=dsrc, recv_boxes=drecv),
         stencils=SimpleNamespace(bookmark=bm, ranks=rk, codes=cd),
     )
+
+
+def near_field(src_points, charges, src_bookmark, nbr_bookmark, nbr_list, recv_points,
+               recv_bookmark) -> np.ndarray:
+    """_ckernels.pyx:290-323 restated (orc_near_field)."""
+    sp = np.ascontiguousarray(src_points, dtype=np.float64).reshape(-1, 3)
+    rp = np.ascontiguousarray(recv_points, dtype=np.float64).reshape(-1, 3)
+    q = np.ascontiguousarray(charges, dtype=np.float64)
+    sbm, nbm, nl, rbm = (np.ascontiguousarray(a, dtype=np.int64)
+                         for a in (src_bookmark, nbr_bookmark, nbr_list, recv_bookmark))
+    phi = np.empty(rp.shape[0], dtype=np.float64)
+    load().orc_near_field(_ptr(sp), _ptr(q), _ptr(sbm), _ptr(nbm), _ptr(nl), _ptr(rp),
+                          _ptr(rbm), max(0, rbm.shape[0] - 1), rp.shape[0], _ptr(phi))
+    return phi
+
+
+def direct(src_points, charges, recv_points) -> np.ndarray:
+    """_ckernels.pyx:326-350 restated (orc_direct)."""
+    sp = np.ascontiguousarray(src_points, dtype=np.float64).reshape(-1, 3)
+    rp = np.ascontiguousarray(recv_points, dtype=np.float64).reshape(-1, 3)
+    q = np.ascontiguousarray(charges, dtype=np.float64)
+    phi = np.empty(rp.shape[0], dtype=np.float64)
+    load().orc_direct(_ptr(sp), _ptr(q), sp.shape[0], _ptr(rp), rp.shape[0], _ptr(phi))
+    return phi

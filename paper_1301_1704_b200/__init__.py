@@ -30,6 +30,7 @@ from .lists import (
     propagate_to_parents,
 )
 from .scan import compact_flags, exclusive_scan
+from .fmm import direct_sum, near_field_potentials
 from .pseudosort import (
     DEFAULT_HISTOGRAM_BUDGET,
     MAX_LEVEL,

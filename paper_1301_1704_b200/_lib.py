@@ -85,6 +85,11 @@ SIGNATURES = [
       C.POINTER(PointSetC), _p, _p]),
     ("fmmb_dist_lists", C.c_int,
      [_p, _p, C.c_int, C.c_uint64, C.c_uint64, ALLOC_FN, _p, C.POINTER(StructuresC), _p]),
+    ("fmmb_near_field", C.c_int,
+     [_p, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p, _p, _i64, _p, _i64, _p, _i64,
+      _p, _i64, _i64, _p, _i64, _p, _p]),
+    ("fmmb_direct_potentials", C.c_int,
+     [_p, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _p, _p]),
 ]
 
 _lib = None
@@ -142,13 +147,14 @@ def handle(dev: torch.device) -> int:
 
 
 SORT_PATHS = {1: "bucket", 2: "onesweep"}
-_SORT_PATH_IDS = {"auto": 0, "bucket": 1, "onesweep": 2}
+_SORT_PATH_IDS = {"auto": 0, "bucket": 1, "onesweep": 2, "bucket_hist": 3}
 
 
 def set_sort_path(path: str, device=None) -> None:
     """Select the sort-phase strategy of the fused build on a device:
-    "auto" (bucket sort, Onesweep rerun on overflow), "bucket" or "onesweep".
-    Both strategies produce bit-identical outputs."""
+    "auto" (bucket sort, Onesweep rerun on overflow), "bucket", "onesweep" or
+    "bucket_hist" (bucket sort without speculative regions: histogram pass
+    first).  All strategies produce bit-identical outputs."""
     if path not in _SORT_PATH_IDS:
         raise ValueError(f"unknown sort path {path!r}")
     dev = device_of(device)

@@ -128,7 +128,7 @@ extern "C" const char* fmmb_last_error(fmmb_handle_t h) {
 extern "C" int64_t fmmb_last_launch_count(fmmb_handle_t h) { return h ? h->launches : -1; }
 
 extern "C" fmmb_status fmmb_set_sort_path(fmmb_handle_t h, int path) {
-  if (!h || path < 0 || path > 2) return FMMB_ERR_ARG;
+  if (!h || path < 0 || path > 3) return FMMB_ERR_ARG;
   h->sort_path = path;
   return FMMB_OK;
 }
@@ -493,7 +493,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
   int64_t launches = 0;
   bool fast = h->sort_path != 2 && tot > 0;
   // speculative bucket regions (no histogram pass) unless this shape missed last time
-  bool spec = fast && spec_possible(bucket_geo(L, n, m, h->num_sms)) &&
+  bool spec = fast && h->sort_path != 3 && spec_possible(bucket_geo(L, n, m, h->num_sms)) &&
               !(h->spec_miss_level == L && h->spec_miss_n == n && h->spec_miss_m == m);
   BuildPlanHost* hp = (BuildPlanHost*)h->pinned;
   ListsParams lp{};
@@ -784,3 +784,4 @@ extern "C" fmmb_status fmmb_sort_points(fmmb_handle_t h, const double* points,
 
 #include "plugin.cuh"
 #include "dist_api.cuh"
+#include "nearfield.cuh"

@@ -256,12 +256,82 @@ def reorder(points, charges, bins, boxes, ranks, max_level: int):
 
 
 # ------------------------------------------------- evaluation (not the path)
-def near_field(*args, **kwargs):
-    raise NotImplementedError("near_field is outside the build path (SURVEY §8(f) row 1)")
+def _f64_col(c, dev):
+    """1-D f64 CUDA view (strided columns of an (N,3) tensor are kept as is)."""
+    if isinstance(c, torch.Tensor) and c.is_cuda and c.dtype == torch.float64 and c.dim() == 1:
+        return c
+    return _host.to_device(c, dev, torch.float64, (-1,))
 
 
-def direct_potentials(*args, **kwargs):
-    raise NotImplementedError("direct_potentials is outside the build path (SURVEY §8(f) row 1)")
+def _strided(c):
+    return [_ptr(c), c.stride(0) if c.numel() else 1]
+
+
+def near_field_device(sx, sy, sz, sq, src_bookmark, nbr_bookmark, nbr_list, rx, ry, rz,
+                      recv_bookmark) -> torch.Tensor:
+    """near_field on CUDA tensors (columns may be strided views); phi f64[M]."""
+    dev = _lib.device_of(sx.device)
+    cols_s = [_f64_col(c, dev) for c in (sx, sy, sz)]
+    cols_r = [_f64_col(c, dev) for c in (rx, ry, rz)]
+    q = _host.to_device(sq, dev, torch.float64, (-1,)) if sq is not None else None
+    sbm, nbm, nl, rbm = (_host.to_device(a, dev, torch.int64, (-1,))
+                         for a in (src_bookmark, nbr_bookmark, nbr_list, recv_bookmark))
+    ns, nr = cols_s[0].numel(), cols_r[0].numel()
+    if cols_s[1].numel() != ns or cols_s[2].numel() != ns or (q is not None and q.numel() != ns):
+        raise DomainError("near_field: source arrays differ in length")
+    if cols_r[1].numel() != nr or cols_r[2].numel() != nr:
+        raise DomainError("near_field: receiver arrays differ in length")
+    if nbm.numel() != rbm.numel():
+        raise DomainError("near_field: neighbour and receiver bookmarks differ in length")
+    phi = torch.empty(nr, dtype=torch.float64, device=dev)
+    kr = max(0, rbm.numel() - 1)
+    _call("fmmb_near_field", dev, *_strided(cols_s[0]), *_strided(cols_s[1]),
+          *_strided(cols_s[2]), _ptr(q) if q is not None else None, ns, _ptr(sbm),
+          max(0, sbm.numel() - 1), _ptr(nbm), _ptr(nl), nl.numel(), *_strided(cols_r[0]),
+          *_strided(cols_r[1]), *_strided(cols_r[2]), nr, _ptr(rbm), kr, _ptr(phi))
+    return phi
+
+
+def near_field(sx, sy, sz, sq, src_bookmark, nbr_bookmark, nbr_list, rx, ry, rz,
+               recv_bookmark):
+    """Near-field direct sums over each receiver box's neighbour segments
+    (_ckernels.pyx:290-323): bit-identical to the compiled backend."""
+    args = (sx, sy, sz, sq, src_bookmark, nbr_bookmark, nbr_list, rx, ry, rz, recv_bookmark)
+    dout = _host.is_device_input(*args)
+    dev = _host.pick_device(*args)
+    kinds = (torch.float64,) * 4 + (torch.int64,) * 3 + (torch.float64,) * 3 + (torch.int64,)
+    cols = [a if (isinstance(a, torch.Tensor) and a.is_cuda) or a is None
+            else _host.to_device(a, dev, k, (-1,)) for a, k in zip(args, kinds)]
+    return _out(near_field_device(*cols), dout)
+
+
+def direct_potentials_device(sx, sy, sz, sq, rx, ry, rz) -> torch.Tensor:
+    dev = _lib.device_of(sx.device)
+    cols_s = [_f64_col(c, dev) for c in (sx, sy, sz)]
+    cols_r = [_f64_col(c, dev) for c in (rx, ry, rz)]
+    q = _host.to_device(sq, dev, torch.float64, (-1,))
+    ns, nr = cols_s[0].numel(), cols_r[0].numel()
+    if cols_s[1].numel() != ns or cols_s[2].numel() != ns or q.numel() != ns:
+        raise DomainError("direct_potentials: source arrays differ in length")
+    if cols_r[1].numel() != nr or cols_r[2].numel() != nr:
+        raise DomainError("direct_potentials: receiver arrays differ in length")
+    phi = torch.empty(nr, dtype=torch.float64, device=dev)
+    _call("fmmb_direct_potentials", dev, *_strided(cols_s[0]), *_strided(cols_s[1]),
+          *_strided(cols_s[2]), _ptr(q), ns, *_strided(cols_r[0]), *_strided(cols_r[1]),
+          *_strided(cols_r[2]), nr, _ptr(phi))
+    return phi
+
+
+def direct_potentials(sx, sy, sz, sq, rx, ry, rz, chunk: int = 1024, threads: int = 1):
+    """Brute-force sums, sequential over sources per receiver
+    (_ckernels.pyx:326-350).  `chunk` / `threads` do not change the result
+    (the reference's receiver blocking / OpenMP width) and are ignored."""
+    args = (sx, sy, sz, sq, rx, ry, rz)
+    dout = _host.is_device_input(*args)
+    dev = _host.pick_device(*args)
+    cols = [a if (isinstance(a, torch.Tensor) and a.is_cuda)
+            else _host.to_device(a, dev, torch.float64, (-1,)) for a in args]
+    return _out(direct_potentials_device(*cols), dout)
 
 
 def install(fmmkit_module=None):

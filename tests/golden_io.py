@@ -81,3 +81,14 @@ def large_inputs(spec: dict):
     src, q, _ = generate(spec["n"], 1, spec["dist"], spec["seed"])
     _, _, recv = generate(1, spec["m"], spec["dist"], spec["seed"] + 1000)
     return src, (q if spec["charges"] else None), recv, spec["level"]
+
+
+def nearfield() -> dict:
+    """phi of the near-field consumer (tests/golden/make_golden_nearfield.py)."""
+    z = np.load(os.path.join(HERE, "nearfield.npz"))
+    return {k: z[k] for k in z.files}
+
+
+def nearfield_hashes() -> dict:
+    with open(os.path.join(HERE, "nearfield_hashes.json")) as f:
+        return json.load(f)

@@ -54,3 +54,27 @@ def test_generate_matches_reference_cli(ref):
         b = ref_generate(RunSpec(n_sources=1000, n_receivers=700, dist=dist, seed=5))
         for x, y in zip(a, b):
             assert np.array_equal(x, y)
+
+
+@pytest.mark.parametrize("name", sorted(gio.small_cases()))
+def test_oracle_near_field_matches_golden(name):
+    """orc_near_field (C restatement of _ckernels.pyx:290-323) on the
+    reference's own sorted outputs reproduces the reference's phi."""
+    case = gio.small_cases()[name]
+    nf = gio.nearfield()
+    out = gio.expected_outputs(case)
+    q = out.get("src.charges", np.ones(out["src.points"].shape[0]))
+    phi = orc.near_field(out["src.points"], q, out["src.bookmarks"], out["neighbor_bookmark"],
+                         out["neighbor_list"], out["recv.points"], out["recv.bookmarks"])
+    assert np.array_equal(phi.view(np.uint64), nf[f"{name}/phi"].view(np.uint64))
+
+
+def test_oracle_direct_matches_golden():
+    nf = gio.nearfield()
+    for name in ("u3_L3", "s5_L5"):
+        src, q, recv, _ = gio.case_inputs(gio.small_cases()[name])
+        assert np.array_equal(orc.direct(src, q, recv).view(np.uint64),
+                              nf[f"{name}/direct"].view(np.uint64))
+    src, q, recv = nf["clustered/in.src"], nf["clustered/in.q"], nf["clustered/in.recv"]
+    assert np.array_equal(orc.direct(src, q, recv).view(np.uint64),
+                          nf["clustered/direct"].view(np.uint64))
