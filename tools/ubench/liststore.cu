@@ -55,6 +55,43 @@ __global__ void k_staged(int64_t* r, int16_t* c, int64_t per_warp) {
     __syncwarp();
   }
 }
+
+// rows of 184 entries produced 23 lanes x 8 chunks into shared memory
+// (st.shared, ranks + codes), flushed by one TMA bulk store per stream per
+// row (cp.async.bulk.global.shared::cta), double-buffered per warp
+__device__ __forceinline__ uint32_t s_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+template <int WARPS>
+__global__ void k_tma(int64_t* r, int16_t* c, int64_t per_warp) {
+  __shared__ __align__(128) int64_t sr[WARPS][2][184];
+  __shared__ __align__(128) int16_t sc[WARPS][2][184];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  int64_t* rp = r + w * per_warp;
+  int16_t* cp = c + w * per_warp;
+  int buf = 0;
+  for (int64_t o = 0; o + 184 <= per_warp; o += 184, buf ^= 1) {
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+    __syncwarp();
+#pragma unroll
+    for (int ch = 0; ch < 8; ++ch)
+      if (lane < 23) {
+        sr[warp][buf][ch * 23 + lane] = o + ch * 23 + lane;
+        sc[warp][buf][ch * 23 + lane] = (int16_t)lane;
+      }
+    __syncwarp();
+    if (lane == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(rp + o),
+                   "r"(s_u32(&sr[warp][buf][0])), "r"(184 * 8) : "memory");
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(cp + o),
+                   "r"(s_u32(&sc[warp][buf][0])), "r"(184 * 2) : "memory");
+      asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+    }
+  }
+  if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
 int main() {
   const int64_t N = (int64_t)1 << 29;  // 4 GiB of i64
   int64_t* r; int16_t* c;
@@ -77,6 +114,7 @@ int main() {
     run("rank+code, 26 lanes", k_stream<26, true, true>, grid, 256, 10.0 * (per / 26 * 26) * warps, r, c, per);
     run("rank 16B vectors", k_stream16, grid, 256, 8.0 * (per / 64 * 64) * warps, r, per);
     run("rank+code staged, 16B flushes", k_staged, grid, 256, 10.0 * (per / 26 * 26) * warps, r, c, per);
+    run("rank+code TMA bulk rows (184)", k_tma<8>, grid, 256, 10.0 * (per / 184 * 184) * warps, r, c, per);
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
 }
