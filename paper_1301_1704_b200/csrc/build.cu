@@ -399,6 +399,9 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
                        cudaStream_t s, bool lists, const DistSortArgs* dsa = nullptr) {
   const int64_t tot = n + m;
   const int stride = L + 1;
+  // level-L occupancy bitmaps + rank directory drive the bucket path's heads
+  // pass: always with lists, and for the partitioned sort (dsa->bmp wanted)
+  const bool heads = lists || (dsa && dsa->bmp);
 
   // bitmap segment layout: seg = set*(L+1)+l, each starting on a rank tile
   RankParams rp{};
@@ -415,7 +418,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
       words += t * kRTileWords;
     }
   rp.tile_off[rp.nseg] = tiles;
-  const int64_t bmp_words = lists ? words : 0, rank_tiles = lists ? tiles : 0;
+  const int64_t bmp_words = heads ? words : 0, rank_tiles = heads ? tiles : 0;
 
   // count-scan tiles: capacity from min(m, 8^(l-1)) receiver parents per level
   int64_t cs_tiles = 1;
@@ -478,16 +481,12 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
   lo.boxes = (uint64_t*)A(a_boxes);
   lo.ne = ne_out;
   lo.bm = bm_out;
-  lo.bmp[0] = lists ? (unsigned long long*)(bmp + rp.word_off[L]) : nullptr;
-  lo.bmp[1] = lists ? (unsigned long long*)(bmp + rp.word_off[stride + L]) : nullptr;
+  lo.bmp[0] = heads ? (unsigned long long*)(bmp + rp.word_off[L]) : nullptr;
+  lo.bmp[1] = heads ? (unsigned long long*)(bmp + rp.word_off[stride + L]) : nullptr;
   lo.kinfo = dplan->kinfo;
   if (dsa) {
     lo.gid[0] = dsa->gid_src;
     lo.gid[1] = dsa->gid_recv;
-    if (dsa->bmp) {
-      lo.bmp[0] = (unsigned long long*)dsa->bmp;
-      lo.bmp[1] = (unsigned long long*)(dsa->bmp + level_words(L));
-    }
   }
 
   int64_t launches = 0;
@@ -502,13 +501,12 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     if (ev) cudaEventRecord(ev[0], s);
     cudaMemsetAsync(ws, 0, zero_bytes, s);
     if (tot == 0) cudaMemsetAsync(bm_out, 0, 2 * sizeof(int64_t), s);
-    if (dsa && dsa->bmp) cudaMemsetAsync(dsa->bmp, 0, 2 * level_words(L) * sizeof(uint64_t), s);
 
     // ---- K1-K4: sort both sets into the reference layout
     BucketRun brun;
     if (tot > 0) {
       const fmmb_status st =
-          fast ? sort_bucket(h, src, q, n, recv, m, L, lo, lists, spec, dplan, s, launches, brun)
+          fast ? sort_bucket(h, src, q, n, recv, m, L, lo, heads, spec, dplan, s, launches, brun)
                : sort_onesweep<KeyT>(h, src, q, n, recv, m, L, lo, dplan, s, launches);
       if (st != FMMB_OK) {
         cudaFreeAsync(ws, s);
@@ -555,12 +553,12 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
         }
         rp.keys_out[set * stride + k] = dst;
       }
-    if (lists) {
+    if (heads) {
       k_rank<<<(unsigned)rank_tiles, kRThreads, 0, s>>>(rp);
       ++launches;
     }
     if (brun.scratch) {  // bucket path: bookmarks / non-empty keys at global box ranks
-      if (lists) {
+      if (heads) {
         HeadsParams hpar{};
         for (int set = 0; set < 2; ++set) {
           hpar.bmp[set] = bmp + rp.word_off[set * stride + L];
@@ -579,6 +577,12 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
         ++launches;
       }
       cudaFreeAsync(brun.scratch, s);
+    }
+    if (dsa && dsa->bmp) {  // this rank's level-L occupancy, for the all-reduce
+      cudaMemcpyAsync(dsa->bmp, bmp + rp.word_off[L], level_words(L) * sizeof(uint64_t),
+                      cudaMemcpyDeviceToDevice, s);
+      cudaMemcpyAsync(dsa->bmp + level_words(L), bmp + rp.word_off[stride + L],
+                      level_words(L) * sizeof(uint64_t), cudaMemcpyDeviceToDevice, s);
     }
     if (ev) cudaEventRecord(ev[2], s);
 
@@ -639,9 +643,9 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
                      "a point's Morton index lies outside the level-%d grid "
                      "(coordinates must lie in the unit cube)", L);
   }
-  const int64_t ks = lists ? hp->ktot[L] : (n > 0 ? hp->kinfo[0] : 0);
-  const int64_t kr = lists ? hp->ktot[stride + L] : (m > 0 ? hp->kinfo[1] - ks : 0);
-  if (lists && tot > 0 && (hp->kinfo[0] != ks || (m > 0 && hp->kinfo[1] != ks + kr))) {
+  const int64_t ks = heads ? hp->ktot[L] : (n > 0 ? hp->kinfo[0] : 0);
+  const int64_t kr = heads ? hp->ktot[stride + L] : (m > 0 ? hp->kinfo[1] - ks : 0);
+  if (heads && tot > 0 && (hp->kinfo[0] != ks || (m > 0 && hp->kinfo[1] != ks + kr))) {
     cudaFreeAsync(ws, s);
     return fmmb_fail(h, FMMB_ERR_CUDA, "internal: box counts disagree (%lld/%lld vs %lld/%lld)",
                      (long long)hp->kinfo[0], (long long)hp->kinfo[1], (long long)ks,

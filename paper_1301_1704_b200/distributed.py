@@ -63,9 +63,16 @@ class Comm:
     def allreduce_sum(self, xs: list) -> list:
         raise NotImplementedError
 
-    def all_to_all(self, chunks: list) -> list:
+    def all_to_all(self, chunks: list, recv_rows: list | None = None) -> list:
         """chunks[i][d] = tensor from driven rank i to rank d; returns
-        out[i][s] = tensor rank ranks[i] received from rank s."""
+        out[i][s] = tensor rank ranks[i] received from rank s.  recv_rows[i][s]
+        (optional) = its row count, when already known (no size exchange)."""
+        raise NotImplementedError
+
+    def exchange_counts(self, counts: list) -> list:
+        """counts[i] = k host ints per destination rank (k*size, destination
+        major) from driven rank i -> out[i][k*s + j] = value j rank ranks[i]
+        got from rank s."""
         raise NotImplementedError
 
     def all_gather(self, xs: list) -> list:
@@ -86,8 +93,13 @@ class SimComm(Comm):
             tot += x
         return [tot.clone() for _ in xs]
 
-    def all_to_all(self, chunks):
+    def all_to_all(self, chunks, recv_rows=None):
         return [[chunks[s][d] for s in range(self.size)] for d in range(self.size)]
+
+    def exchange_counts(self, counts):
+        k = len(counts[0]) // self.size
+        return [[counts[s][k * d + j] for s in range(self.size) for j in range(k)]
+                for d in range(self.size)]
 
     def all_gather(self, xs):
         return [list(xs) for _ in xs]
@@ -115,18 +127,25 @@ class TorchComm(Comm):
         self.dist.all_reduce(y, group=self.group)
         return [y.to(x.device)]
 
-    def all_to_all(self, chunks):
+    def exchange_counts(self, counts):
+        (row,) = counts
+        x = torch.tensor([int(c) for c in row], dtype=torch.int64)
+        if not self.stage:
+            x = x.cuda()
+        y = torch.empty_like(x)
+        self.dist.all_to_all_single(y, x, group=self.group)
+        return [[int(v) for v in y.cpu().tolist()]]
+
+    def all_to_all(self, chunks, recv_rows=None):
         (row,) = chunks
         dev = row[0].device
         dtype = row[0].dtype
         tail = tuple(row[0].shape[1:])
         width = int(np.prod(tail)) if tail else 1
-        sizes = torch.tensor([int(c.shape[0]) for c in row], dtype=torch.int64)
-        if not self.stage:
-            sizes = sizes.to(dev)
-        rsizes = torch.empty_like(sizes)
-        self.dist.all_to_all_single(rsizes, sizes, group=self.group)
-        rs = rsizes.cpu().tolist()
+        if recv_rows is not None:
+            rs = [int(v) for v in recv_rows[0]]
+        else:
+            rs = self.exchange_counts([[int(c.shape[0]) for c in row]])[0]
         send = self._to(torch.cat([c.reshape(-1) for c in row]))
         recv = torch.empty(sum(rs) * width, dtype=dtype, device=send.device)
         self.dist.all_to_all_single(recv, send, [r * width for r in rs],
@@ -318,6 +337,31 @@ class DistShard:
             exchanged=dict(self.exchanged))
 
 
+def _cat(parts: list) -> torch.Tensor:
+    """torch.cat of received pieces; no copy when they are already adjacent
+    slices of one receive buffer (TorchComm) or a single piece."""
+    if len(parts) == 1:
+        return parts[0]
+    p0 = parts[0]
+    at = p0.data_ptr()
+    adjacent = all(t.is_contiguous() and t.dtype == p0.dtype for t in parts)
+    for t in parts:
+        if not adjacent:
+            break
+        if t.numel() and t.data_ptr() != at:
+            adjacent = False
+        at += t.numel() * t.element_size()
+    if adjacent and p0.untyped_storage().data_ptr() <= p0.data_ptr():
+        rows = sum(int(t.shape[0]) for t in parts)
+        base = p0.untyped_storage()
+        off = (p0.data_ptr() - base.data_ptr()) // p0.element_size()
+        full = torch.empty(0, dtype=p0.dtype, device=p0.device).set_(
+            base, off, (rows,) + tuple(p0.shape[1:]), p0.stride())
+        if all(t.untyped_storage().data_ptr() == base.data_ptr() for t in parts):
+            return full
+    return torch.cat(parts)
+
+
 def _shard_csr(bm: torch.Tensor, offset: int, last: bool) -> torch.Tensor:
     x = bm + offset
     return x if last else x[:-1]
@@ -362,20 +406,27 @@ def build_all_distributed(shards: list, max_level: int, comm: Comm, ops=None,
         return out
 
     with_q = shards[0][1] is not None
+    # one count exchange (src and recv counts per destination), then the five
+    # payload exchanges with known sizes: no host round trip between them
+    cnt = comm.exchange_counts([[v for d in range(P) for v in (pk[5][d], pk[6][d])]
+                                for pk in packs])
+    rsrc = [[c[2 * s] for s in range(P)] for c in cnt]
+    rrecv = [[c[2 * s + 1] for s in range(P)] for c in cnt]
     ex = {}
-    for key, idx, cidx in (("sxyz", 0, 5), ("sgid", 2, 5), ("rxyz", 3, 6), ("rgid", 4, 6)):
-        ex[key] = comm.all_to_all([split(pk[idx], pk[cidx]) for pk in packs])
+    for key, idx, cidx, rr in (("sxyz", 0, 5, rsrc), ("sgid", 2, 5, rsrc), ("rxyz", 3, 6, rrecv),
+                               ("rgid", 4, 6, rrecv)):
+        ex[key] = comm.all_to_all([split(pk[idx], pk[cidx]) for pk in packs], rr)
     if with_q:
-        ex["sq"] = comm.all_to_all([split(pk[1], pk[5]) for pk in packs])
+        ex["sq"] = comm.all_to_all([split(pk[1], pk[5]) for pk in packs], rsrc)
     results = []
     sorted_sets = []
     bmps = []
     for i, r in enumerate(comm.ranks):
-        src = torch.cat(ex["sxyz"][i]) if ex["sxyz"][i] else torch.empty((0, 3), dtype=torch.float64, device=dev[i])
-        sgid = torch.cat(ex["sgid"][i])
-        rxyz = torch.cat(ex["rxyz"][i])
-        rgid = torch.cat(ex["rgid"][i])
-        q = torch.cat(ex["sq"][i]) if with_q else None
+        src = _cat(ex["sxyz"][i])
+        sgid = _cat(ex["sgid"][i])
+        rxyz = _cat(ex["rxyz"][i])
+        rgid = _cat(ex["rgid"][i])
+        q = _cat(ex["sq"][i]) if with_q else None
         sent = sum(int(t.shape[0]) for d, t in enumerate(split(packs[i][0], packs[i][5])) if d != r)
         sent_r = sum(int(t.shape[0]) for d, t in enumerate(split(packs[i][3], packs[i][6])) if d != r)
         # 4. local sort phase
@@ -388,12 +439,12 @@ def build_all_distributed(shards: list, max_level: int, comm: Comm, ops=None,
     # 6. owned lists
     lists = [ops.dist_lists(gbmps[i], L, *windows[r]) for i, r in enumerate(comm.ranks)]
     # 7. global offsets from every rank's shard sizes
-    def stats(i):
+    def stats(i):  # host-known sizes (a CSR's last bookmark is its list length)
         ss, sr = sorted_sets[i]
         dl = lists[i]
-        v = [ss.points.shape[0], sr.points.shape[0], dl.neighbor_bookmark[-1]]
+        v = [ss.points.shape[0], sr.points.shape[0], dl.neighbor_list.shape[0]]
         for l in range(2, L + 1):
-            v.append(dl.st_bookmark[l][-1])
+            v.append(dl.st_ranks[l].shape[0])
         return torch.tensor([int(x) for x in v], dtype=torch.int64, device=dev[i])
 
     allst = comm.all_gather([stats(i) for i in range(nd)])
