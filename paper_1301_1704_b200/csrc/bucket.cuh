@@ -1026,6 +1026,37 @@ __global__ void __launch_bounds__(kLcThreads)
   }  // final buckets
 }
 
+// perm[p] = gid[perm[p]] of its set (multi-GPU: local -> global input index);
+// four independent gathers in flight per thread
+__global__ void __launch_bounds__(256)
+    k_gid_map(int64_t* __restrict__ perm, int64_t n, int64_t m, const int64_t* __restrict__ g0,
+              const int64_t* __restrict__ g1, const uint32_t* __restrict__ fail) {
+  if (__ldg(fail)) return;  // the sort reruns on the general path
+  const int64_t tot = n + m;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x * 4 + threadIdx.x; b < tot; b += stride) {
+    int64_t v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t p = b + (int64_t)k * blockDim.x;
+      v[k] = p < tot ? perm[p] : 0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t p = b + (int64_t)k * blockDim.x;
+      if (p < tot) {
+        const int64_t* g = p < n ? g0 : g1;
+        v[k] = g ? __ldg(g + v[k]) : v[k];
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t p = b + (int64_t)k * blockDim.x;
+      if (p < tot) perm[p] = v[k];
+    }
+  }
+}
+
 // Bookmarks and non-empty keys at their global box ranks (HEADS variant):
 // one warp per bucket walks the bucket's words of the level-L bitmap; the
 // h-th set bit is the bucket's h-th box, its rank = rank directory + prefix

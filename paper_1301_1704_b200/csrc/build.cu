@@ -309,8 +309,13 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
   }
   const uint32_t* lfail = spec ? &dplan->spec_fail : po.fail;
   const bool ck32 = g.shift + g.cbits <= 32;
-#define FMMB_LOCAL(CK, NW, HD)                                                             \
-  launch_local<CK, NW, HD>(h, rec, idx, po.bstart_f, rbase, po.desc, po.nfinal, g, L, o, lst, \
+  // multi-GPU: the local pass writes local input indices; their global
+  // indices follow in one high-occupancy gather (k_gid_map) instead of
+  // latency-exposed lookups inside the local pass
+  LocalOut ol = o;
+  ol.gid[0] = ol.gid[1] = nullptr;
+#define FMMB_LOCAL(CK, NW, HD)                                                              \
+  launch_local<CK, NW, HD>(h, rec, idx, po.bstart_f, rbase, po.desc, po.nfinal, g, L, ol, lst, \
                            lfail, s)
   if (heads) {
     if (narrow) { if (ck32) FMMB_LOCAL(uint32_t, true, true); else FMMB_LOCAL(uint64_t, true, true); }
@@ -321,6 +326,10 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
   }
 #undef FMMB_LOCAL
   launches += 6;
+  if (o.gid[0] || o.gid[1]) {
+    k_gid_map<<<(unsigned)h->num_sms * 16, 256, 0, s>>>(o.perm, n, m, o.gid[0], o.gid[1], lfail);
+    ++launches;
+  }
   run.scratch = w;
   run.g = g;
   run.bstart_f = po.bstart_f;

@@ -31,7 +31,9 @@ __device__ __forceinline__ uint32_t part_bin(const double* src, const double* re
   return (uint32_t)((key & ((1ull << sbits) - 1ull)) >> (sbits - pbits));
 }
 
-__global__ void __launch_bounds__(kPartThreads)
+constexpr int kPartHistThreads = 1024;  // 2 CTAs (64 KiB counters each) fill an SM
+
+__global__ void __launch_bounds__(kPartHistThreads)
     k_part_hist(const double* __restrict__ src, int64_t n, const double* __restrict__ recv,
                 int64_t m, int level, int pbits, uint32_t* __restrict__ hist,
                 uint32_t* __restrict__ err) {
@@ -72,7 +74,10 @@ __global__ void __launch_bounds__(kPartThreads)
   const int64_t base = (int64_t)blockIdx.x * kPartTile;
   for (int k = 0; k < kPartItems; ++k) {
     const int64_t i = base + k * kPartThreads + threadIdx.x;
-    if (i < tot) atomicAdd(&s_c[part_slot(src, recv, n, i, level, pbits, bin_rank, nranks)], 1u);
+    const int sl = i < tot ? part_slot(src, recv, n, i, level, pbits, bin_rank, nranks) : -1;
+    // warp-aggregated: few destinations, so most lanes share a counter
+    const unsigned peers = __match_any_sync(0xffffffffu, sl);
+    if (sl >= 0 && (threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(&s_c[sl], (uint32_t)__popc(peers));
   }
   __syncthreads();
   for (int sl = threadIdx.x; sl < nslots; sl += blockDim.x)

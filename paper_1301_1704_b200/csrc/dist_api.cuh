@@ -23,8 +23,9 @@ extern "C" fmmb_status fmmb_part_histogram(fmmb_handle_t h, const double* src, i
   cudaMemsetAsync(err, 0, 4, s);
   cudaMemsetAsync(hist, 0, sizeof(uint32_t) << pbits, s);
   if (n + m > 0) {
-    const int grid = (int)std::min<int64_t>(ceil_div(n + m, kPartThreads), (int64_t)h->num_sms * 4);
-    k_part_hist<<<grid, kPartThreads, sizeof(uint32_t) << pbits, s>>>(src, n, recv, m, level,
+    const int grid =
+        (int)std::min<int64_t>(ceil_div(n + m, kPartHistThreads), (int64_t)h->num_sms * 2);
+    k_part_hist<<<grid, kPartHistThreads, sizeof(uint32_t) << pbits, s>>>(src, n, recv, m, level,
                                                                        pbits, hist, err);
     ++h->launches;
   }
