@@ -26,9 +26,12 @@ from .lists import (
     build_level_directory,
     build_neighbor_table,
     build_translation_stencils,
+    dump_structures,
     gather_adjacent_sources,
+    load_structures,
     propagate_to_parents,
 )
+from . import container
 from .scan import compact_flags, exclusive_scan
 from .fmm import direct_sum, near_field_potentials
 from .pseudosort import (

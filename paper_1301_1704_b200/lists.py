@@ -380,3 +380,76 @@ def build_translation_stencils(directory: LevelDirectory) -> TranslationStencils
         ranks[level] = rk
         codes[level] = cd
     return TranslationStencils(bookmark=bookmark, ranks=ranks, codes=codes)
+
+
+# ------------------------------------------------------- FMMS dump / load
+def _point_set_arrays(ps: SortedPointSet, prefix: str) -> dict:
+    """lists.py:190-200 (same names and order)."""
+    arrays = {
+        f"{prefix}_points": ps.points,
+        f"{prefix}_permutation": ps.permutation,
+        f"{prefix}_bookmarks": ps.bookmarks,
+        f"{prefix}_non_empty": ps.non_empty_index,
+        f"{prefix}_boxes": ps.boxes,
+    }
+    if ps.charges is not None:
+        arrays[f"{prefix}_charges"] = ps.charges
+    return arrays
+
+
+def dump_structures(structures: FmmStructures, path) -> None:
+    """Write the CORE / LVLS / STNC container of lists.py:203-219, byte-
+    identical to the reference; device-resident structures are streamed out
+    of HBM in chunks (container.write_container)."""
+    from . import container
+
+    L = structures.max_level
+    core = container.Section(tag="CORE", meta={"max_level": L})
+    core.arrays.update(_point_set_arrays(structures.sorted_src, "src"))
+    core.arrays.update(_point_set_arrays(structures.sorted_recv, "recv"))
+    core.arrays["neighbor_bookmark"] = structures.neighbor_table.neighbor_bookmark
+    core.arrays["neighbor_list"] = structures.neighbor_table.neighbor_list
+    lvls = container.Section(tag="LVLS", meta={"max_level": L})
+    for level in range(2, L + 1):
+        lvls.arrays[f"src_{level}"] = structures.directory.src_boxes[level]
+        lvls.arrays[f"recv_{level}"] = structures.directory.recv_boxes[level]
+    stnc = container.Section(tag="STNC")
+    for level in range(2, L + 1):
+        stnc.arrays[f"bookmark_{level}"] = structures.stencils.bookmark[level]
+        stnc.arrays[f"ranks_{level}"] = structures.stencils.ranks[level]
+        stnc.arrays[f"codes_{level}"] = structures.stencils.codes[level]
+    container.write_container(path, L, [core, lvls, stnc])
+
+
+def load_structures(path, device=None) -> FmmStructures:
+    """lists.py:234-257; with `device` the arrays are uploaded to it."""
+    from . import container
+
+    max_level, sections = container.read_container(path, device=device)
+    by_tag = {s.tag: s for s in sections}
+    core, lvls, stnc = by_tag["CORE"], by_tag["LVLS"], by_tag["STNC"]
+    L = max_level
+    directory = LevelDirectory(
+        max_level=L,
+        src_boxes={l: lvls.arrays[f"src_{l}"] for l in range(2, L + 1)},
+        recv_boxes={l: lvls.arrays[f"recv_{l}"] for l in range(2, L + 1)},
+    )
+    stencils = TranslationStencils(
+        bookmark={l: stnc.arrays[f"bookmark_{l}"] for l in range(2, L + 1)},
+        ranks={l: stnc.arrays[f"ranks_{l}"] for l in range(2, L + 1)},
+        codes={l: stnc.arrays[f"codes_{l}"] for l in range(2, L + 1)},
+    )
+
+    def ps(prefix):
+        a = core.arrays
+        return SortedPointSet(level=L, points=a[f"{prefix}_points"],
+                              charges=a.get(f"{prefix}_charges"),
+                              permutation=a[f"{prefix}_permutation"],
+                              bookmarks=a[f"{prefix}_bookmarks"],
+                              non_empty_index=a[f"{prefix}_non_empty"], boxes=a[f"{prefix}_boxes"])
+
+    return FmmStructures(
+        max_level=L, sorted_src=ps("src"), sorted_recv=ps("recv"),
+        neighbor_table=NeighborTable(neighbor_bookmark=core.arrays["neighbor_bookmark"],
+                                     neighbor_list=core.arrays["neighbor_list"]),
+        directory=directory, stencils=stencils)

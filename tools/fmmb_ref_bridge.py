@@ -3,7 +3,8 @@
 Loaded with `-p fmmb_ref_bridge` before collection: binds the B200 kernel
 plugin as `fmmkit.backend.kernels` (the reference's own swap mechanism,
 cli.py:263-266) and replaces the build API entry points the tests import
-(`from fmmkit import build_all, sort_points, ...`) with the device versions.
+(`from fmmkit import build_all, sort_points, ...`), the scan, the FMMS
+container IO and dump/load_structures with the device versions.
 Test infrastructure only.
 """
 
@@ -30,6 +31,18 @@ import fmmkit.scan as _scan  # noqa: E402
 for _name in ("exclusive_scan", "compact_flags"):  # scan.py:25-81 -> device scan
     setattr(fmmkit, _name, getattr(fb, _name))
     setattr(_scan, _name, getattr(fb, _name))
+
+import fmmkit.container as _container  # noqa: E402
+
+from paper_1301_1704_b200 import container as _our_container  # noqa: E402
+
+for _name in ("Section", "write_container", "read_container"):  # container.py -> streaming IO
+    setattr(_container, _name, getattr(_our_container, _name))
+for _name in ("dump_structures", "load_structures"):  # lists.py:203-257
+    setattr(fmmkit, _name, getattr(fb, _name))
+    setattr(_lists, _name, getattr(fb, _name))
+# near_field_potentials / direct_sum (fmm.py) reach the device through the
+# bound plugin: kernels.near_field / kernels.direct_potentials
 
 CALLS = {"build_all": 0}
 _orig_build_all = fb.build_all
