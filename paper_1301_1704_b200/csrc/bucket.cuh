@@ -482,6 +482,7 @@ struct FinalMap {  // coarse bucket (+ next kRefBits key bits) -> final bucket
   uint32_t spec_cap;   // speculative regions: spec_cap slots apart, `cap` usable (0: exact starts)
   uint32_t* spec_fail; // raised when a region overflows
   uint32_t* err;       // speculative mode: out-of-grid keys (the skipped histogram pass checks them)
+  unsigned long long* bmp[2];  // level-L occupancy bits set here when non-null
 };
 
 template <bool NARROW>
@@ -563,6 +564,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
         encode_any<NARROW>(xyz[3 * tid], xyz[3 * tid + 1], xyz[3 * tid + 2], level, grid);
     if (fm.err && raw > kmask) atomicOr(fm.err, 1u);
     const uint64_t key = raw & kmask;
+    if (fm.bmp[0]) atomicOr(fm.bmp[i >= n ? 1 : 0] + (key >> 6), 1ull << (key & 63));
     uint32_t b = bucket_of(key, i >= n, g);
     if (refined)
       b = __ldg(fm.fbase + b) +

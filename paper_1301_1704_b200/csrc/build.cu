@@ -63,6 +63,21 @@ extern "C" fmmb_status fmmb_create(int device, fmmb_handle_t* out) {
     delete h;
     return FMMB_ERR_CUDA;
   }
+  {
+    cudaStream_t side;
+    cudaEvent_t e[3];
+    if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaFreeHost(h->pinned);
+      delete h;
+      return FMMB_ERR_CUDA;
+    }
+    for (auto& x : e) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
+    h->side = side;
+    h->ev_split = e[0];
+    h->ev_rank = e[1];
+    h->ev_side = e[2];
+    h->overlap = getenv("FMMB_NO_OVERLAP") == nullptr;
+  }
   // stream-ordered pool: keep freed workspace for reuse across calls
   cudaMemPool_t pool;
   if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
@@ -117,6 +132,9 @@ extern "C" fmmb_status fmmb_destroy(fmmb_handle_t h) {
   if (!h) return FMMB_ERR_ARG;
   cudaSetDevice(h->device);
   if (h->pinned) cudaFreeHost(h->pinned);
+  if (h->side) cudaStreamDestroy((cudaStream_t)h->side);
+  for (void* e : {h->ev_split, h->ev_rank, h->ev_side})
+    if (e) cudaEventDestroy((cudaEvent_t)e);
   delete h;
   return FMMB_OK;
 }
@@ -209,11 +227,15 @@ template <bool NARROW>
 void launch_spec(const double* src, const double* q, const double* recv, const BucketGeo& g,
                  int num_sms, int L, uint32_t* counts, uint32_t* bstart, uint64_t* sst,
                  uint32_t* ctl, uint32_t* rbase, const PlanOut& po, double* rec, uint32_t* idx,
-                 uint32_t* spec_fail, uint32_t* err, cudaStream_t s) {
+                 uint32_t* spec_fail, uint32_t* err, cudaStream_t s,
+                 unsigned long long* const* sbmp) {
   const unsigned nbg = (unsigned)ceil_div(g.nb, 256);
   k_spec_init<<<nbg, 256, 0, s>>>(g, kSpecStride, po.cursor, rbase, po.desc, po.nfinal);
   const int sgrid = (int)std::min<int64_t>(num_sms, ceil_div(g.n + g.m, kSRows));
-  const FinalMap fm{po.fbase, po.gtab, ctl + 4, kLcCap, (uint32_t)kSpecStride, spec_fail, err};
+  FinalMap fm{po.fbase, po.gtab, ctl + 4, kLcCap, (uint32_t)kSpecStride, spec_fail, err,
+              {nullptr, nullptr}};
+  fm.bmp[0] = sbmp[0];
+  fm.bmp[1] = sbmp[1];
   k_bkt_scatter<NARROW><<<(unsigned)sgrid, kSThreads, scatter_smem_bytes(), s>>>(
       src, q, recv, g, L, scatter_rows_per_cta(g.n + g.m, sgrid), po.cursor, rec, idx, fm);
   k_spec_counts<<<nbg, 256, 0, s>>>(g, kSpecStride, po.cursor, counts);
@@ -227,7 +249,7 @@ template <bool NARROW>
 void launch_hs(const double* src, const double* q, const double* recv, const BucketGeo& g,
                int num_sms, int L, uint32_t* mat, uint32_t* bstart, uint64_t* sst, uint32_t* ctl,
                uint32_t* fine, const PlanOut& po, double* rec, uint32_t* idx, uint32_t* err,
-               cudaStream_t s) {
+               cudaStream_t s, unsigned long long* const* sbmp) {
   k_bkt_hist<NARROW><<<(unsigned)g.hgrid, kHThreads, (size_t)g.nb * 4, s>>>(src, recv, g, L,
                                                                              mat, err);
   k_bkt_scan<<<(unsigned)ceil_div(g.nb, kScanBuckets), 256, 0, s>>>(mat, g, bstart, sst,
@@ -235,7 +257,7 @@ void launch_hs(const double* src, const double* q, const double* recv, const Buc
   k_bkt_fine<NARROW><<<num_sms * 8, 256, 0, s>>>(src, recv, g, L, bstart, ctl + 2, kLcCap, fine);
   k_bkt_plan<<<(unsigned)ceil_div(g.nb, 256), 256, 0, s>>>(g, bstart, ctl + 2, kLcCap, fine, po);
   const int sgrid = (int)std::min<int64_t>(num_sms, ceil_div(g.n + g.m, kSRows));
-  const FinalMap fm{po.fbase, po.gtab, ctl + 2, kLcCap, 0u, nullptr, nullptr};
+  const FinalMap fm{po.fbase, po.gtab, ctl + 2, kLcCap, 0u, nullptr, nullptr, {sbmp[0], sbmp[1]}};
   k_bkt_scatter<NARROW><<<(unsigned)sgrid, kSThreads, scatter_smem_bytes(), s>>>(
       src, q, recv, g, L, scatter_rows_per_cta(g.n + g.m, sgrid), po.cursor, rec, idx, fm);
 }
@@ -246,7 +268,7 @@ inline bool spec_possible(const BucketGeo& g) { return g.shift <= kLcSmallBits; 
 fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int64_t n,
                         const double* recv, int64_t m, int L, const LocalOut& o, bool heads,
                         bool spec, BuildPlanHost* dplan, cudaStream_t s, int64_t& launches,
-                        BucketRun& run) {
+                        BucketRun& run, cudaStream_t ls) {
   const BucketGeo g = bucket_geo(L, n, m, h->num_sms);
   const int64_t tot = n + m;
   const int64_t nfcap = final_buckets_cap(g, kLcCap);
@@ -295,18 +317,20 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
   if (spec) {  // no histogram pass: fixed regions, exact starts from the final cursors
     if (narrow)
       launch_spec<true>(src, q, recv, g, h->num_sms, L, mat, bstart, sst, ctl, rbase, po, rec,
-                        idx, &dplan->spec_fail, &dplan->err, s);
+                        idx, &dplan->spec_fail, &dplan->err, s, o.bmp);
     else
       launch_spec<false>(src, q, recv, g, h->num_sms, L, mat, bstart, sst, ctl, rbase, po, rec,
-                         idx, &dplan->spec_fail, &dplan->err, s);
+                         idx, &dplan->spec_fail, &dplan->err, s, o.bmp);
     po.bstart_f = bstart;
   } else if (narrow) {
     launch_hs<true>(src, q, recv, g, h->num_sms, L, mat, bstart, sst, ctl, fine, po, rec, idx,
-                    &dplan->err, s);
+                    &dplan->err, s, o.bmp);
   } else {
     launch_hs<false>(src, q, recv, g, h->num_sms, L, mat, bstart, sst, ctl, fine, po, rec, idx,
-                     &dplan->err, s);
+                     &dplan->err, s, o.bmp);
   }
+  // the scatter set the occupancy bits: from here the local pass (on `ls`)
+  // and the caller's stream (directory, lists) proceed independently
   const uint32_t* lfail = spec ? &dplan->spec_fail : po.fail;
   const bool ck32 = g.shift + g.cbits <= 32;
   // multi-GPU: the local pass writes local input indices; their global
@@ -314,22 +338,30 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
   // latency-exposed lookups inside the local pass
   LocalOut ol = o;
   ol.gid[0] = ol.gid[1] = nullptr;
-#define FMMB_LOCAL(CK, NW, HD)                                                              \
-  launch_local<CK, NW, HD>(h, rec, idx, po.bstart_f, rbase, po.desc, po.nfinal, g, L, ol, lst, \
-                           lfail, s)
-  if (heads) {
-    if (narrow) { if (ck32) FMMB_LOCAL(uint32_t, true, true); else FMMB_LOCAL(uint64_t, true, true); }
-    else { if (ck32) FMMB_LOCAL(uint32_t, false, true); else FMMB_LOCAL(uint64_t, false, true); }
-  } else {
-    if (narrow) { if (ck32) FMMB_LOCAL(uint32_t, true, false); else FMMB_LOCAL(uint64_t, true, false); }
-    else { if (ck32) FMMB_LOCAL(uint32_t, false, false); else FMMB_LOCAL(uint64_t, false, false); }
-  }
+  ol.bmp[0] = ol.bmp[1] = nullptr;  // bits already set by the scatter
+  const PlanOut pl = po;
+  auto local = [=](cudaStream_t st) {
+#define FMMB_LOCAL(CK, NW, HD)                                                                 \
+  launch_local<CK, NW, HD>(h, rec, idx, pl.bstart_f, rbase, pl.desc, pl.nfinal, g, L, ol, lst, \
+                           lfail, st)
+    if (heads) {
+      if (narrow) { if (ck32) FMMB_LOCAL(uint32_t, true, true); else FMMB_LOCAL(uint64_t, true, true); }
+      else { if (ck32) FMMB_LOCAL(uint32_t, false, true); else FMMB_LOCAL(uint64_t, false, true); }
+    } else {
+      if (narrow) { if (ck32) FMMB_LOCAL(uint32_t, true, false); else FMMB_LOCAL(uint64_t, true, false); }
+      else { if (ck32) FMMB_LOCAL(uint32_t, false, false); else FMMB_LOCAL(uint64_t, false, false); }
+    }
 #undef FMMB_LOCAL
-  launches += 6;
-  if (o.gid[0] || o.gid[1]) {
-    k_gid_map<<<(unsigned)h->num_sms * 16, 256, 0, s>>>(o.perm, n, m, o.gid[0], o.gid[1], lfail);
-    ++launches;
+    if (o.gid[0] || o.gid[1])
+      k_gid_map<<<(unsigned)h->num_sms * 16, 256, 0, st>>>(o.perm, n, m, o.gid[0], o.gid[1],
+                                                            lfail);
+  };
+  launches += 6 + ((o.gid[0] || o.gid[1]) ? 1 : 0);
+  if (ls != s) {  // right after the scatter: overlaps the directory, the count and the write
+    cudaEventRecord((cudaEvent_t)h->ev_split, s);
+    cudaStreamWaitEvent(ls, (cudaEvent_t)h->ev_split, 0);
   }
+  local(ls);
   run.scratch = w;
   run.g = g;
   run.bstart_f = po.bstart_f;
@@ -506,6 +538,12 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
   BuildPlanHost* hp = (BuildPlanHost*)h->pinned;
   ListsParams lp{};
   int64_t nwork_cap = 0;
+  // local pass + heads stream (== s unless the bucket path overlaps them
+  // with the directory / lists); join() orders s after its work
+  cudaStream_t ls = s;
+  auto join = [&]() {
+    if (ls != s) cudaStreamWaitEvent(s, (cudaEvent_t)h->ev_side, 0);
+  };
   for (int attempt = 0;; ++attempt) {
     if (ev) cudaEventRecord(ev[0], s);
     cudaMemsetAsync(ws, 0, zero_bytes, s);
@@ -513,11 +551,14 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
 
     // ---- K1-K4: sort both sets into the reference layout
     BucketRun brun;
+    ls = (fast && heads && h->overlap && h->side) ? (cudaStream_t)h->side : s;
     if (tot > 0) {
       const fmmb_status st =
-          fast ? sort_bucket(h, src, q, n, recv, m, L, lo, heads, spec, dplan, s, launches, brun)
+          fast ? sort_bucket(h, src, q, n, recv, m, L, lo, heads, spec, dplan, s, launches, brun,
+                             ls)
                : sort_onesweep<KeyT>(h, src, q, n, recv, m, L, lo, dplan, s, launches);
       if (st != FMMB_OK) {
+        join();
         cudaFreeAsync(ws, s);
         return st;
       }
@@ -566,27 +607,6 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
       k_rank<<<(unsigned)rank_tiles, kRThreads, 0, s>>>(rp);
       ++launches;
     }
-    if (brun.scratch) {  // bucket path: bookmarks / non-empty keys at global box ranks
-      if (heads) {
-        HeadsParams hpar{};
-        for (int set = 0; set < 2; ++set) {
-          hpar.bmp[set] = bmp + rp.word_off[set * stride + L];
-          hpar.dir[set] = dir + rp.word_off[set * stride + L];
-        }
-        hpar.ktot_src = dplan->ktot + L;
-        hpar.ktot_recv = dplan->ktot + stride + L;
-        hpar.bstart = brun.bstart_f;
-        hpar.rbase = brun.rbase;
-        hpar.hpos = brun.hpos;
-        hpar.ne = ne_out;
-        hpar.bm = bm_out;
-        hpar.kinfo = dplan->kinfo;
-        k_bkt_heads<<<(unsigned)h->num_sms * 8, 256, 0, s>>>(hpar, brun.desc, brun.nfinal,
-                                                              brun.g);
-        ++launches;
-      }
-      cudaFreeAsync(brun.scratch, s);
-    }
     if (dsa && dsa->bmp) {  // this rank's level-L occupancy, for the all-reduce
       cudaMemcpyAsync(dsa->bmp, bmp + rp.word_off[L], level_words(L) * sizeof(uint64_t),
                       cudaMemcpyDeviceToDevice, s);
@@ -618,16 +638,44 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
           lp, glay, (uint64_t*)W(o_st4), (uint64_t*)W(o_st2), tc + 10, dplan->seg_totals);
       launches += 2;
     }
+    if (brun.scratch) {  // bucket path: bookmarks / non-empty keys at global box ranks
+      if (ls != s) {  // heads on the side stream: after the local pass and the rank directory
+        cudaEventRecord((cudaEvent_t)h->ev_rank, s);
+        cudaStreamWaitEvent(ls, (cudaEvent_t)h->ev_rank, 0);
+      }
+      if (heads) {
+        HeadsParams hpar{};
+        for (int set = 0; set < 2; ++set) {
+          hpar.bmp[set] = bmp + rp.word_off[set * stride + L];
+          hpar.dir[set] = dir + rp.word_off[set * stride + L];
+        }
+        hpar.ktot_src = dplan->ktot + L;
+        hpar.ktot_recv = dplan->ktot + stride + L;
+        hpar.bstart = brun.bstart_f;
+        hpar.rbase = brun.rbase;
+        hpar.hpos = brun.hpos;
+        hpar.ne = ne_out;
+        hpar.bm = bm_out;
+        hpar.kinfo = dplan->kinfo;
+        k_bkt_heads<<<(unsigned)h->num_sms * 8, 256, 0, ls>>>(hpar, brun.desc, brun.nfinal,
+                                                               brun.g);
+        ++launches;
+      }
+      cudaFreeAsync(brun.scratch, ls);
+    }
+    if (ls != s) cudaEventRecord((cudaEvent_t)h->ev_side, ls);
     if (ev) cudaEventRecord(ev[3], s);
 
     // ---- sizes back to the host (the build's single synchronisation)
     cudaMemcpyAsync(hp, dplan, sizeof(BuildPlanHost), cudaMemcpyDeviceToHost, s);
     cudaError_t ce = cudaStreamSynchronize(s);
     if (ce != cudaSuccess) {
+      join();
       cudaFreeAsync(ws, s);
       return fmmb_fail(h, FMMB_ERR_CUDA, "build phase A failed: %s", cudaGetErrorString(ce));
     }
     if (spec && hp->spec_fail && attempt < 2) {  // a speculative region overflowed
+      join();
       h->spec_miss_level = L;
       h->spec_miss_n = n;
       h->spec_miss_m = m;
@@ -635,6 +683,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
       continue;
     }
     if (hp->fail && fast && attempt < 2) {  // a bucket overflowed: general sort
+      join();
       fast = false;
       spec = false;
       continue;
@@ -642,11 +691,13 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     break;
   }
   if (hp->fail) {
+    join();
     cudaFreeAsync(ws, s);
     return fmmb_fail(h, FMMB_ERR_CUDA, "internal: bucket sort overflow after fallback");
   }
   h->last_sort_path = fast ? 1 : 2;
   if (hp->err) {
+    join();
     cudaFreeAsync(ws, s);
     return fmmb_fail(h, FMMB_ERR_DOMAIN,
                      "a point's Morton index lies outside the level-%d grid "
@@ -654,7 +705,10 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
   }
   const int64_t ks = heads ? hp->ktot[L] : (n > 0 ? hp->kinfo[0] : 0);
   const int64_t kr = heads ? hp->ktot[stride + L] : (m > 0 ? hp->kinfo[1] - ks : 0);
-  if (heads && tot > 0 && (hp->kinfo[0] != ks || (m > 0 && hp->kinfo[1] != ks + kr))) {
+  // (kinfo comes from the heads pass; overlapped, it is not read back yet)
+  if (heads && ls == s && tot > 0 &&
+      (hp->kinfo[0] != ks || (m > 0 && hp->kinfo[1] != ks + kr))) {
+    join();
     cudaFreeAsync(ws, s);
     return fmmb_fail(h, FMMB_ERR_CUDA, "internal: box counts disagree (%lld/%lld vs %lld/%lld)",
                      (long long)hp->kinfo[0], (long long)hp->kinfo[1], (long long)ks,
@@ -693,6 +747,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     }
     char* arena_b = (char*)alloc(ctx, std::max<size_t>(b.off, 256));
     if (!arena_b) {
+      join();
       cudaFreeAsync(ws, s);
       return fmmb_fail(h, FMMB_ERR_ALLOC, "list allocation of %zu bytes failed", b.off);
     }
@@ -727,6 +782,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
       out->n_st[k] = hp->seg_totals[k];
     }
   }
+  join();  // the caller's stream sees the local pass and heads complete
   if (ev) {
     if (!lists) cudaEventRecord(ev[4], s);
     cudaEventRecord(ev[5], s);

@@ -16,6 +16,14 @@ struct fmmb_handle_s {
   // geometry (level, n, m) whose speculative bucket regions last overflowed:
   // the next build of the same shape starts with the histogram pass
   int64_t spec_miss_level = -1, spec_miss_n = -1, spec_miss_m = -1;
+  // side stream of the bucket path: the local pass + heads run there while
+  // the caller's stream builds the directory and the lists (both only need
+  // the occupancy bitmaps, which the scatter sets)
+  void* side = nullptr;          // cudaStream_t
+  void* ev_split = nullptr;      // cudaEvent_t: scatter done (caller stream)
+  void* ev_rank = nullptr;       // rank directory done (caller stream)
+  void* ev_side = nullptr;       // side stream's work done
+  bool overlap = true;           // FMMB_NO_OVERLAP=1 serialises (A/B)
   std::string err;
 };
 
