@@ -52,6 +52,7 @@ def parse():
     p.add_argument("--e2e-steps", type=int, default=3)
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-nf", action="store_true", help="skip the near-field consumer timing")
     p.add_argument("--sort-path", default="auto",
                    choices=["auto", "bucket", "onesweep", "bucket_hist"])
     return p.parse_args()
@@ -301,6 +302,31 @@ def run_ours(args):
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": statistics.median(times) * 1e3}
 
+    # ---- the near-field pass consuming the device-built
+    # structures in place (not part of the build metric; reported beside it)
+    nf = None
+    if not args.no_nf and rank == 0 and args.workload != "c4":
+        st = step()
+        ss, sr, nt = st.sorted_src, st.sorted_recv, st.neighbor_table
+        cs = torch.nn.functional.pad(torch.cumsum(torch.diff(ss.bookmarks)[nt.neighbor_list], 0),
+                                     (1, 0))
+        pairs = int(((cs[nt.neighbor_bookmark[1:]] - cs[nt.neighbor_bookmark[:-1]])
+                     * torch.diff(sr.bookmarks)).sum())
+        fb.near_field_potentials(st)
+        nts = []
+        for _ in range(3):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            fb.near_field_potentials(st)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            nts.append(e0.elapsed_time(e1) * 1e-3)
+        t_nf = statistics.median(nts)
+        nf = {"kernel": "k_near_field", "pair_interactions": pairs, "ms": t_nf * 1e3,
+              "interactions_per_s": pairs / t_nf, "dtype": "f64 (bit-exact vs compiled reference)"}
+        st = None
+
     cpu = None
     if not args.no_cpu and rank == 0:
         rate, kind, cores, sample, _ = cpu_reference_rate()
@@ -336,6 +362,7 @@ def run_ours(args):
             "e2e": e2e,
             "cpu_baseline": cpu,
             "gpu_launches": int(launches),
+            "near_field": nf,
         }
         print(json.dumps(line), flush=True)
     if dist is not None:

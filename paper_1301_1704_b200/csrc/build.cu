@@ -761,6 +761,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     if (ev) cudaEventRecord(ev[4], s);
     k_lists_write<<<lgrid, kLThreads, 0, s>>>(lp, (const ListsLayout*)W(o_lay));
     ++launches;
+    if (ev) cudaEventRecord(ev[5], s);  // the write kernel alone (before the side join)
 
     out->neighbor_bookmark = lp.bm[0];
     out->neighbor_list = lp.ranks_out[0];
@@ -784,8 +785,10 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
   }
   join();  // the caller's stream sees the local pass and heads complete
   if (ev) {
-    if (!lists) cudaEventRecord(ev[4], s);
-    cudaEventRecord(ev[5], s);
+    if (!lists) {
+      cudaEventRecord(ev[4], s);
+      cudaEventRecord(ev[5], s);
+    }
   }
   cudaFreeAsync(ws, s);
   out->n_launches = launches;
