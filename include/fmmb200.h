@@ -286,6 +286,18 @@ FMMB_API fmmb_status fmmb_direct_potentials(fmmb_handle_t h, const double* sx,
                                    const double* ry, int64_t ry_stride, const double* rz,
                                    int64_t rz_stride, int64_t nr, double* phi, void* stream);
 
+/* classify(node, global_src_boxes, plan) for ONE level (boxtype.py:103-144,
+ * stencil owners :63-101): types[i] in {0 DOMESTIC, 1 EXPORT, 2 IMPORT,
+ * 3 ROOT, 4 OTHER} of the global non-empty source box boxes[i] at `level`
+ * for `node`, given the partition-level owner-unit table box_proc_id
+ * (8^partition_level entries, int32).  FMMB_ERR_DOMAIN for level < 2 and
+ * for levels the reference cannot resolve to one unit. */
+FMMB_API fmmb_status fmmb_classify_boxes(fmmb_handle_t h, const uint64_t* boxes, int64_t n,
+                                int level, const int32_t* box_proc_id,
+                                int64_t n_units_table, int partition_level,
+                                int critical_level, int nodes, int units_per_node, int node,
+                                int8_t* types, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

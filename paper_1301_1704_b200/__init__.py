@@ -32,6 +32,7 @@ from .lists import (
     propagate_to_parents,
 )
 from . import container
+from .boxtype import BoxType, TypedBoxList, classify
 from .scan import compact_flags, exclusive_scan
 from .fmm import direct_sum, near_field_potentials
 from .pseudosort import (

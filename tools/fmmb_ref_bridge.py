@@ -41,6 +41,13 @@ for _name in ("Section", "write_container", "read_container"):  # container.py -
 for _name in ("dump_structures", "load_structures"):  # lists.py:203-257
     setattr(fmmkit, _name, getattr(fb, _name))
     setattr(_lists, _name, getattr(fb, _name))
+import fmmkit.boxtype as _boxtype  # noqa: E402
+
+from paper_1301_1704_b200 import boxtype as _our_boxtype  # noqa: E402
+
+for _name in ("classify", "dump_typed", "load_typed"):  # boxtype.py -> device classify
+    setattr(_boxtype, _name, getattr(_our_boxtype, _name))
+fmmkit.classify = _our_boxtype.classify
 # near_field_potentials / direct_sum (fmm.py) reach the device through the
 # bound plugin: kernels.near_field / kernels.direct_potentials
 
