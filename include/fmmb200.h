@@ -298,6 +298,17 @@ FMMB_API fmmb_status fmmb_classify_boxes(fmmb_handle_t h, const uint64_t* boxes,
                                 int critical_level, int nodes, int units_per_node, int node,
                                 int8_t* types, void* stream);
 
+/* One candidate level of choose_partition (partition.py:74-127): the dense
+ * load of `level` (recv_counts of the boxes at from_level summed into their
+ * level-`level` ancestors), its inclusive prefix incl, and for k = 0..units
+ * bounds[k] (0, searchsorted_left(incl, total*k/units) + 1 capped at 8^level,
+ * 8^level) and cum[k] = incl[bounds[k] - 1] (0 for bounds 0).  bounds and cum
+ * are caller-allocated (units + 1). */
+FMMB_API fmmb_status fmmb_partition_level(fmmb_handle_t h, const uint64_t* recv_boxes,
+                                 const int64_t* recv_counts, int64_t n, int from_level,
+                                 int level, int64_t total, int units, int64_t* bounds,
+                                 int64_t* cum, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

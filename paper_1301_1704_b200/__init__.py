@@ -33,6 +33,7 @@ from .lists import (
 )
 from . import container
 from .boxtype import BoxType, TypedBoxList, classify
+from .partition import PartitionPlan, choose_partition
 from .scan import compact_flags, exclusive_scan
 from .fmm import direct_sum, near_field_potentials
 from .pseudosort import (

@@ -90,6 +90,8 @@ SIGNATURES = [
       _p, _i64, _i64, _p, _i64, _p, _p]),
     ("fmmb_classify_boxes", C.c_int,
      [_p, _p, _i64, C.c_int, _p, _i64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, _p, _p]),
+    ("fmmb_partition_level", C.c_int,
+     [_p, _p, _p, _i64, C.c_int, C.c_int, _i64, C.c_int, _p, _p, _p]),
     ("fmmb_direct_potentials", C.c_int,
      [_p, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _p, _i64, _i64, _p, _p]),
 ]

@@ -858,3 +858,4 @@ extern "C" fmmb_status fmmb_sort_points(fmmb_handle_t h, const double* points,
 #include "dist_api.cuh"
 #include "nearfield.cuh"
 #include "boxtype.cuh"
+#include "partplan.cuh"

@@ -1,7 +1,7 @@
 """The reference's OWN tests (oracle/_ref/tests, unmodified) run against this
 framework through tools/fmmb_ref_bridge.py: test_lists.py, test_pseudosort.py,
 test_morton.py, test_scan.py, test_container.py, test_fmm.py (near field and
-direct sums through the bound plugin), test_boxtype.py and acceptance criteria 1-3."""
+direct sums through the bound plugin), test_boxtype.py, test_partition.py and acceptance criteria 1-3."""
 
 import os
 import subprocess
@@ -23,6 +23,7 @@ REF = os.path.join(ROOT, "oracle", "_ref")
     "tests/test_container.py",
     "tests/test_fmm.py",
     "tests/test_boxtype.py",
+    "tests/test_partition.py",
     "tests/test_acceptance.py::test_criterion_1_list_correctness",
     "tests/test_acceptance.py::test_criterion_2_single_count_coverage",
     "tests/test_acceptance.py::test_criterion_3_pseudo_sort_contract",

@@ -48,6 +48,14 @@ from paper_1301_1704_b200 import boxtype as _our_boxtype  # noqa: E402
 for _name in ("classify", "dump_typed", "load_typed"):  # boxtype.py -> device classify
     setattr(_boxtype, _name, getattr(_our_boxtype, _name))
 fmmkit.classify = _our_boxtype.classify
+
+import fmmkit.partition as _partition  # noqa: E402
+
+from paper_1301_1704_b200 import partition as _our_partition  # noqa: E402
+
+for _name in ("choose_partition", "dump_plan", "load_plan"):  # partition.py:74-257
+    setattr(_partition, _name, getattr(_our_partition, _name))
+fmmkit.choose_partition = _our_partition.choose_partition
 # near_field_potentials / direct_sum (fmm.py) reach the device through the
 # bound plugin: kernels.near_field / kernels.direct_potentials
 
