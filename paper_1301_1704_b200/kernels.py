@@ -43,13 +43,20 @@ def _ptr(t: torch.Tensor):
 
 
 # ----------------------------------------------------------- bit dilation
+def _shape(a) -> tuple:
+    """Elementwise plugin functions keep the input's shape (numpy semantics
+    of _pykernels.py:22-57, e.g. (B, 27) candidate grids in partition.py)."""
+    return tuple(a.shape) if hasattr(a, "shape") else tuple(np.shape(a))
+
+
 def _unary_u64(fn_name: str, v):
     dev = _host.pick_device(v)
     dout = _host.is_device_input(v)
+    shp = _shape(v)
     x = _dev_u64(v, dev)
     o = torch.empty_like(x)
     _call(fn_name, dev, _ptr(x), x.numel(), _ptr(o))
-    return _out(o, dout)
+    return _out(o.reshape(shp), dout)
 
 
 def spread_bits(v):
@@ -66,23 +73,24 @@ def interleave_coords(ix, iy, iz):
     """Morton index from box coordinates (_pykernels.py:43-48)."""
     dev = _host.pick_device(ix, iy, iz)
     dout = _host.is_device_input(ix, iy, iz)
-    xs = [_dev_u64(a, dev) for a in (ix, iy, iz)]
+    shp = np.broadcast_shapes(_shape(ix), _shape(iy), _shape(iz))
+    xs = [_dev_u64(np.broadcast_to(a, shp) if not isinstance(a, torch.Tensor) else
+                   a.expand(shp), dev) for a in (ix, iy, iz)]
     n = xs[0].numel()
-    if any(t.numel() != n for t in xs):
-        raise DomainError("interleave_coords: coordinate arrays differ in length")
     o = torch.empty(n, dtype=torch.uint64, device=dev)
     _call("fmmb_interleave_coords", dev, *[_ptr(t) for t in xs], n, _ptr(o))
-    return _out(o, dout)
+    return _out(o.reshape(shp), dout)
 
 
 def deinterleave_indices(idx):
     """(ix, iy, iz) from Morton indices (_pykernels.py:51-57)."""
     dev = _host.pick_device(idx)
     dout = _host.is_device_input(idx)
+    shp = _shape(idx)
     k = _dev_u64(idx, dev)
     outs = [torch.empty_like(k) for _ in range(3)]
     _call("fmmb_deinterleave_indices", dev, _ptr(k), k.numel(), *[_ptr(t) for t in outs])
-    return tuple(_out(t, dout) for t in outs)
+    return tuple(_out(t.reshape(shp), dout) for t in outs)
 
 
 # --------------------------------------------------------------- encoding
@@ -108,10 +116,11 @@ def encode_points(x, y, z, level: int):
     (_ckernels.pyx:85-104): truncating f64 quantisation, upper clamp."""
     dev = _host.pick_device(x, y, z)
     dout = _host.is_device_input(x, y, z)
+    shp = _shape(x)
     cols = [_host.to_device(c, dev, torch.float64, (-1,)) for c in (x, y, z)]
     if not (cols[0].numel() == cols[1].numel() == cols[2].numel()):
         raise DomainError("encode_points: coordinate arrays differ in length")
-    return _out(encode_points_device(*cols, level), dout)
+    return _out(encode_points_device(*cols, level).reshape(shp), dout)
 
 
 # ---------------------------------------------------------- rank assignment
