@@ -18,7 +18,7 @@ from .errors import CapacityError, DomainError, NativeError
 
 MAX_LEVEL = 20
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libfmmb200.so")
+LIB_PATH = os.environ.get("FMMB_LIB") or os.path.join(_HERE, "libfmmb200.so")  # FMMB_LIB: A/B builds
 
 OK, ERR_DOMAIN, ERR_CAPACITY, ERR_CUDA, ERR_ALLOC, ERR_ARG = range(6)
 

@@ -459,9 +459,14 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // their consumers with plain loads instead.
 constexpr int kSThreads = 1024;
 constexpr int kSRows = kSThreads;   // one row per thread per stage
-constexpr int kSStages = 6;
-constexpr int kSLead = 3;           // stages in flight ahead of the claim
-constexpr int kSDepth = 2;          // stages between claim and store
+#ifndef FMMB_SLEAD  // scatter pipeline shape (overridable for measurement builds)
+#define FMMB_SLEAD 3
+#define FMMB_SDEPTH 2
+#define FMMB_SSTAGES 6
+#endif
+constexpr int kSStages = FMMB_SSTAGES;
+constexpr int kSLead = FMMB_SLEAD;    // stages in flight ahead of the claim
+constexpr int kSDepth = FMMB_SDEPTH;  // stages between claim and store
 static_assert(kSLead + kSDepth + 1 <= kSStages, "ring too small");
 constexpr int kSStageBytes = kSRows * 32;  // xyz (24 B) + q (8 B) per row
 
@@ -588,17 +593,17 @@ __global__ void __launch_bounds__(kSThreads, 1)
   };
   if (tid == 0)
     for (int k = 0; k < kSLead && k < nst; ++k) produce(k);
-  uint32_t d0 = 0, d1 = 0, d2 = 0;
-  // step k: produce k+lead, claim k, store k-2 (slots rotate through d0, d1, d2)
+  // step k: produce k+lead, claim k, store k-depth; the slots of the last
+  // depth+1 stages rotate through static registers (loop unrolled by depth+1)
+  uint32_t d[kSDepth + 1] = {};
   auto step = [&](int k, uint32_t& dk, uint32_t dold) {
     if (tid == 0 && k + kSLead < nst) produce(k + kSLead);
     if (k < nst) dk = claim(k);
     if (k >= kSDepth && k - kSDepth < nst) store(k - kSDepth, dold);
   };
-  for (int k = 0; k < nst + kSDepth; k += 3) {  // unrolled by three: static slot registers
-    step(k, d0, d1);
-    step(k + 1, d1, d2);
-    step(k + 2, d2, d0);
+  for (int k = 0; k < nst + kSDepth; k += kSDepth + 1) {
+#pragma unroll
+    for (int j = 0; j <= kSDepth; ++j) step(k + j, d[j], d[(j + 1) % (kSDepth + 1)]);
   }
 }
 
