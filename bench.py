@@ -70,7 +70,7 @@ def dist_env():
 CPU_SAMPLE = {"n": 2**21, "level": 6, "dist": "uniform", "seed": 1}
 
 
-def cpu_reference_rate(max_seconds: float = 25.0, steps: int | None = None):
+def cpu_reference_rate(max_seconds: float = 25.0, steps: int | None = None, warmup: int = 0):
     """Reference CPU build_all on a bounded sample of the workload: N=M=2^21
     uniform at L=6 (8 points per finest box, the c2 occupancy).  Returns
     (particles/s, kind, cores, sample, per-step rates)."""
@@ -93,6 +93,8 @@ def cpu_reference_rate(max_seconds: float = 25.0, steps: int | None = None):
 
         kind = "port"
         run = lambda: orc.build_all(src, q, recv, L)  # noqa: E731
+    for _ in range(warmup):  # untimed
+        run()
     rates = []
     t_start = time.perf_counter()
     while True:
@@ -115,13 +117,14 @@ def run_reference_arm(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    for _ in range(max(0, min(args.warmup, 1))):
-        pass
-    rate, kind, cores, sample, rates = cpu_reference_rate(steps=max(1, args.steps))
+    # the deterministic reference build is single-threaded (no
+    # threading outside mode="atomic", whose within-box order differs)
+    wu = max(0, min(args.warmup, 3))
+    rate, kind, cores, sample, rates = cpu_reference_rate(steps=max(1, args.steps), warmup=wu)
     dt = 2 * CPU_SAMPLE["n"] / rate
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": len(rates), "warmup": 0,
+        "n_gpus": args.gpus, "steps": len(rates), "warmup": wu,
         "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{args.workload} (bounded CPU sample)", "sample": sample},
