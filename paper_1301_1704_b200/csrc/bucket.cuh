@@ -569,7 +569,10 @@ __global__ void __launch_bounds__(kSThreads, 1)
         encode_any<NARROW>(xyz[3 * tid], xyz[3 * tid + 1], xyz[3 * tid + 2], level, grid);
     if (fm.err && raw > kmask) atomicOr(fm.err, 1u);
     const uint64_t key = raw & kmask;
-    if (fm.bmp[0]) atomicOr(fm.bmp[i >= n ? 1 : 0] + (key >> 6), 1ull << (key & 63));
+    if (fm.bmp[0]) {  // occupancy bit: fire-and-forget global reduction (no return)
+      unsigned long long* w = fm.bmp[i >= n ? 1 : 0] + (key >> 6);
+      asm volatile("red.global.or.b64 [%0], %1;" ::"l"(w), "l"(1ull << (key & 63)) : "memory");
+    }
     uint32_t b = bucket_of(key, i >= n, g);
     if (refined)
       b = __ldg(fm.fbase + b) +
