@@ -77,6 +77,11 @@ FMMB_API int64_t fmmb_last_launch_count(fmmb_handle_t h);
  * fmmb_last_sort_path() reports the path the last build completed on (1/2). */
 FMMB_API fmmb_status fmmb_set_sort_path(fmmb_handle_t h, int path);
 FMMB_API int fmmb_last_sort_path(fmmb_handle_t h);
+/* Bucket path stream structure: 1 (default) = the local pass and the heads
+ * pass run on an internal side stream, concurrently with the directory and
+ * the lists on the caller's stream (joined before the call returns);
+ * 0 = everything in order on the caller's stream.  Outputs are identical. */
+FMMB_API fmmb_status fmmb_set_overlap(fmmb_handle_t h, int on);
 
 /* ------------------------------------------------------ kernel plugin level */
 

@@ -59,6 +59,7 @@ SIGNATURES = [
     ("fmmb_last_launch_count", _i64, [_p]),
     ("fmmb_set_sort_path", C.c_int, [_p, C.c_int]),
     ("fmmb_last_sort_path", C.c_int, [_p]),
+    ("fmmb_set_overlap", C.c_int, [_p, C.c_int]),
     ("fmmb_spread_bits", C.c_int, [_p, _p, _i64, _p, _p]),
     ("fmmb_compact_bits", C.c_int, [_p, _p, _i64, _p, _p]),
     ("fmmb_interleave_coords", C.c_int, [_p, _p, _p, _p, _i64, _p, _p]),
@@ -165,6 +166,14 @@ def set_sort_path(path: str, device=None) -> None:
     h = handle(dev)
     st = load().fmmb_set_sort_path(h, _SORT_PATH_IDS[path])
     check(st, h)
+
+
+def set_overlap(on: bool, device=None) -> None:
+    """Run the bucket path's local + heads passes on a side stream overlapping
+    the directory and lists (default) or serially on the caller's stream."""
+    dev = device_of(device)
+    h = handle(dev)
+    check(load().fmmb_set_overlap(h, 1 if on else 0), h)
 
 
 def stream_of(dev: torch.device) -> int:

@@ -153,6 +153,12 @@ extern "C" fmmb_status fmmb_set_sort_path(fmmb_handle_t h, int path) {
 
 extern "C" int fmmb_last_sort_path(fmmb_handle_t h) { return h ? h->last_sort_path : -1; }
 
+extern "C" fmmb_status fmmb_set_overlap(fmmb_handle_t h, int on) {
+  if (!h) return FMMB_ERR_ARG;
+  h->overlap = on != 0;
+  return FMMB_OK;
+}
+
 int lists_lmin_host(int L) { return L >= 2 ? 2 : L; }
 
 // --------------------------------------------------------------- arenas --

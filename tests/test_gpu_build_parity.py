@@ -30,12 +30,19 @@ CASES = [
 ]
 
 
-@pytest.fixture(params=["auto", "onesweep"])
+@pytest.fixture(params=["auto", "onesweep", "bucket_hist", "serial"])
 def sort_path(request, gpu):
-    """Both sort-phase strategies (bucket sort with overflow rerun, Onesweep)."""
-    gpu._lib.set_sort_path(request.param)
+    """Every sort-phase strategy: bucket sort (speculative regions, overflow
+    rerun) with the local pass overlapped on the side stream, Onesweep, the
+    histogram-sized bucket path, and the bucket path serialised on one stream."""
+    if request.param == "serial":
+        gpu._lib.set_overlap(False)
+        gpu._lib.set_sort_path("auto")
+    else:
+        gpu._lib.set_sort_path(request.param)
     yield request.param
     gpu._lib.set_sort_path("auto")
+    gpu._lib.set_overlap(True)
 
 
 @pytest.mark.parametrize("n,m,level,dist,seed", CASES)
