@@ -611,7 +611,10 @@ __global__ void __launch_bounds__(kSThreads, 1)
 }
 
 // ------------------------------------------------------------ local pass --
-constexpr int kLcWarps = 8;
+#ifndef FMMB_LCWARPS
+#define FMMB_LCWARPS 8
+#endif
+constexpr int kLcWarps = FMMB_LCWARPS;
 constexpr int kLcThreads = kLcWarps * 32;
 constexpr int kLcDigit = 8;  // digit bits per in-smem LSD pass (fallback path)
 constexpr int kLcBins = 1 << kLcDigit;
@@ -623,7 +626,7 @@ template <typename CK>
 __host__ __device__ constexpr size_t lc_smem_bytes() {
   // records | idx | composite x2 | slot x2 | per-warp digit counters | misc
   return (size_t)kLcCap * (32 + 4 + 2 * sizeof(CK) + 2 * 2) +
-         (size_t)kLcWarps * kLcBins * 4 + 128;
+         (size_t)kLcWarps * kLcBins * 4 + 32 + 8 * kLcWarps + 64;
 }
 
 // One stable counting pass over digit [ds, ds+db) of B keys: warps own
@@ -854,13 +857,13 @@ __global__ void __launch_bounds__(kLcThreads)
     cmax = __reduce_max_sync(0xffffffffu, cmax);
     if (lane == 0) {
       s_red[warp] = wt;
-      s_red[8 + warp] = cmax;
+      s_red[kLcWarps + warp] = cmax;
     }
     __syncthreads();
     uint32_t mx = 0;
     for (int i = 0; i < kLcWarps; ++i) {
       x += i < warp ? s_red[i] : 0u;
-      mx = s_red[8 + i] > mx ? s_red[8 + i] : mx;
+      mx = s_red[kLcWarps + i] > mx ? s_red[kLcWarps + i] : mx;
     }
     ranked = mx <= 64;
     uint32_t start = x & 0xFFFFu, hidx = x >> 16;
@@ -981,12 +984,12 @@ __global__ void __launch_bounds__(kLcThreads)
       head = j == 0 || (uint64_t)(kc[j - 1] >> wb) != lk;
     }
     const unsigned hb = __ballot_sync(0xffffffffu, head);
-    if (lane == 0) s_red[8 + warp] = __popc(hb);
+    if (lane == 0) s_red[kLcWarps + warp] = __popc(hb);
     __syncthreads();
     uint32_t woff = 0, ctot = 0;
 #pragma unroll
     for (int i = 0; i < kLcWarps; ++i) {
-      const uint32_t c = s_red[8 + i];
+      const uint32_t c = s_red[kLcWarps + i];
       woff += i < warp ? c : 0u;
       ctot += c;
     }
