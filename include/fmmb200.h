@@ -260,6 +260,28 @@ FMMB_API fmmb_status fmmb_dist_lists(fmmb_handle_t h, const uint64_t* gbmp, int 
                             uint64_t key_lo, uint64_t key_hi, fmmb_alloc_fn alloc, void* ctx,
                             fmmb_structures* out, void* stream);
 
+/* Fused pack + exchange over peer memory (multi-GPU without a separate
+ * all-to-all).  fmmb_part_counts: counts[set * nranks + r] of this rank's
+ * points per destination rank (as fmmb_part_pack reports them), so every
+ * rank can size its receive arrays.  fmmb_part_pack_peer: the same stable
+ * partition, each point stored directly into destination r's arrays
+ * sxyz[r] (n_r x 3), sq[r] (or NULL), sgid[r], rxyz[r], rgid[r] -- device
+ * pointers valid on this device (peer-mapped with CUDA IPC / P2P, or the
+ * same device) -- starting at element soff[r] / roff[r] (this rank's block
+ * at r: the counts of lower source ranks).  Ends with a system-scope fence;
+ * the caller synchronises the stream and barriers before the receivers read. */
+FMMB_API fmmb_status fmmb_part_counts(fmmb_handle_t h, const double* src, int64_t n,
+                             const double* recv, int64_t m, int level, int pbits,
+                             const uint32_t* bin_rank, int nranks, int64_t* counts,
+                             void* stream);
+FMMB_API fmmb_status fmmb_part_pack_peer(fmmb_handle_t h, const double* src, const double* q,
+                                int64_t n, const double* recv, int64_t m, int level, int pbits,
+                                const uint32_t* bin_rank, int nranks, int64_t gbase_src,
+                                int64_t gbase_recv, double* const* sxyz, double* const* sq,
+                                int64_t* const* sgid, double* const* rxyz,
+                                int64_t* const* rgid, const int64_t* soff, const int64_t* roff,
+                                void* stream);
+
 /* ------------------------------------------- consumers of the structures */
 
 /* near_field(sx, sy, sz, sq, src_bookmark, nbr_bookmark, nbr_list, rx, ry,

@@ -81,6 +81,12 @@ SIGNATURES = [
     ("fmmb_part_pack", C.c_int,
      [_p, _p, _p, _i64, _p, _i64, C.c_int, C.c_int, _p, C.c_int, _i64, _i64, _p, _p, _p, _p,
       _p, C.POINTER(_i64), _p]),
+    ("fmmb_part_counts", C.c_int,
+     [_p, _p, _i64, _p, _i64, C.c_int, C.c_int, _p, C.c_int, C.POINTER(_i64), _p]),
+    ("fmmb_part_pack_peer", C.c_int,
+     [_p, _p, _p, _i64, _p, _i64, C.c_int, C.c_int, _p, C.c_int, _i64, _i64,
+      C.POINTER(_p), C.POINTER(_p), C.POINTER(_p), C.POINTER(_p), C.POINTER(_p),
+      C.POINTER(_i64), C.POINTER(_i64), _p]),
     ("fmmb_dist_sort", C.c_int,
      [_p, _p, _p, _i64, _p, _p, _i64, _p, C.c_int, ALLOC_FN, _p, C.POINTER(PointSetC),
       C.POINTER(PointSetC), _p, _p]),

@@ -84,6 +84,19 @@ __global__ void __launch_bounds__(kPartThreads)
     cnt[(int64_t)sl * ntiles + blockIdx.x] = s_c[sl];
 }
 
+// Fused pack + exchange: each point is stored straight into its destination
+// rank's receive arrays (peer memory mapped over NVLink; the same device for
+// simulated ranks) at that rank's offset for this source rank's block.
+struct PeerOut {
+  double* sxyz[kPartMaxRanks];
+  double* sq[kPartMaxRanks];
+  int64_t* sgid[kPartMaxRanks];
+  double* rxyz[kPartMaxRanks];
+  int64_t* rgid[kPartMaxRanks];
+  int64_t soff[kPartMaxRanks];  // element offset of this rank's block at each destination
+  int64_t roff[kPartMaxRanks];
+};
+
 struct PartOut {
   double* sxyz;   // (n, 3) sources grouped by destination
   double* sq;     // (n,) or null
@@ -97,11 +110,13 @@ struct PartOut {
 // points of slot s start at off[s * ntiles + t]; inside the tile each warp
 // owns 128 consecutive points (4 rounds of 32, in order) and ranks lanes
 // with match.any; warps are ordered through per-warp slot counts.
+template <bool PEER>
 __global__ void __launch_bounds__(kPartThreads)
     k_part_scatter(const double* __restrict__ src, const double* __restrict__ q, int64_t n,
                    const double* __restrict__ recv, int64_t m, int level, int pbits,
                    const uint32_t* __restrict__ bin_rank, int nranks,
-                   const int64_t* __restrict__ off, int64_t ntiles, const PartOut o) {
+                   const int64_t* __restrict__ off, int64_t ntiles, const PartOut o,
+                   const __grid_constant__ PeerOut po) {
   constexpr int kW = kPartThreads / 32;
   __shared__ uint32_t s_wc[kW][2 * kPartMaxRanks];
   const int nslots = 2 * nranks;
@@ -144,6 +159,27 @@ __global__ void __launch_bounds__(kPartThreads)
     const int64_t i = wbase + k * 32 + lane;
     if (sl[k] < 0) continue;
     const int64_t dst = off[(int64_t)sl[k] * ntiles + blockIdx.x] + s_wc[warp][sl[k]] + rk[k];
+    if (PEER) {  // position inside the destination's group -> peer arrays
+      const int dr = sl[k] % nranks;
+      const int64_t j = dst - off[(int64_t)sl[k] * ntiles];
+      if (i < n) {
+        const double* p = src + 3 * i;
+        double* x = po.sxyz[dr] + 3 * (po.soff[dr] + j);
+        x[0] = p[0];
+        x[1] = p[1];
+        x[2] = p[2];
+        if (po.sq[dr]) po.sq[dr][po.soff[dr] + j] = q[i];
+        po.sgid[dr][po.soff[dr] + j] = o.gbase_src + i;
+      } else {
+        const double* p = recv + 3 * (i - n);
+        double* x = po.rxyz[dr] + 3 * (po.roff[dr] + j);
+        x[0] = p[0];
+        x[1] = p[1];
+        x[2] = p[2];
+        po.rgid[dr][po.roff[dr] + j] = o.gbase_recv + (i - n);
+      }
+      continue;
+    }
     if (i < n) {
       const double* p = src + 3 * i;
       o.sxyz[3 * dst] = p[0];
@@ -160,6 +196,7 @@ __global__ void __launch_bounds__(kPartThreads)
       o.rgid[d] = o.gbase_recv + (i - n);
     }
   }
+  if (PEER) __threadfence_system();  // peer stores visible before the host-side barrier
 }
 
 }  // namespace fmmb

@@ -72,8 +72,9 @@ extern "C" fmmb_status fmmb_part_pack(fmmb_handle_t h, const double* src, const 
     return cuda_status(h, "part_pack scan");
   if (tot > 0) {
     PartOut o{sxyz, sq, sgid, rxyz, rgid, gbase_src, gbase_recv};
-    k_part_scatter<<<(unsigned)ntiles, kPartThreads, 0, s>>>(src, q, n, recv, m, level, pbits,
-                                                             bin_rank, nranks, off, ntiles, o);
+    PeerOut none{};
+    k_part_scatter<false><<<(unsigned)ntiles, kPartThreads, 0, s>>>(
+        src, q, n, recv, m, level, pbits, bin_rank, nranks, off, ntiles, o, none);
     ++h->launches;
   }
   // per-slot totals = column sums of the slot-major count matrix
@@ -89,6 +90,93 @@ extern "C" fmmb_status fmmb_part_pack(fmmb_handle_t h, const double* src, const 
     counts[sl] = end - hp[sl];
   }
   return cuda_status(h, "part_pack");
+}
+
+// Counts only (no scatter): counts[slot] for slot = set * nranks + rank, so the
+// receivers can size their arrays before the fused pack + exchange.
+// mode 0: counts;  mode 1: scatter into peers (PeerOut from the host tables)
+static fmmb_status part_pass(fmmb_handle_t h, const double* src, const double* q, int64_t n,
+                             const double* recv, int64_t m, int level, int pbits,
+                             const uint32_t* bin_rank, int nranks, int64_t gbase_src,
+                             int64_t gbase_recv, const PeerOut* peers, int64_t* counts,
+                             cudaStream_t s) {
+  using namespace fmmb;
+  if (!h || !bin_rank) return FMMB_ERR_ARG;
+  if (nranks < 1 || nranks > kPartMaxRanks)
+    return fmmb_fail(h, FMMB_ERR_ARG, "nranks %d outside [1, %d]", nranks, kPartMaxRanks);
+  if (level < 1 || level > kMaxLevel || pbits < 1 || pbits > kPartMaxBits || pbits > 3 * level)
+    return fmmb_fail(h, FMMB_ERR_ARG, "invalid level / partition bits");
+  cudaSetDevice(h->device);
+  h->launches = 0;
+  const int64_t tot = n + m;
+  const int nslots = 2 * nranks;
+  const int64_t ntiles = std::max<int64_t>(1, ceil_div(tot, kPartTile));
+  Workspace ws(s);
+  if (!ws.reserve(2 * slice(nslots * ntiles + 1, 8) +
+                  slice(ceil_div(nslots * ntiles, kXTile) + 1, 8) + 8192))
+    return fmmb_fail(h, FMMB_ERR_CUDA, "workspace allocation failed");
+  int64_t* cnt = ws.take<int64_t>(nslots * ntiles);
+  int64_t* off = ws.take<int64_t>(nslots * ntiles + 1);
+  cudaMemsetAsync(cnt, 0, (size_t)nslots * ntiles * 8, s);
+  if (tot > 0) {
+    k_part_count<<<(unsigned)ntiles, kPartThreads, 0, s>>>(src, n, recv, m, level, pbits,
+                                                           bin_rank, nranks, cnt, ntiles);
+    ++h->launches;
+  }
+  ScanResult sr;
+  if (!scan_i64(h, ws, cnt, nslots * ntiles, off, false, &sr, &h->launches))
+    return cuda_status(h, "part scan");
+  if (peers) {
+    if (tot > 0) {
+      PartOut o{nullptr, nullptr, nullptr, nullptr, nullptr, gbase_src, gbase_recv};
+      k_part_scatter<true><<<(unsigned)ntiles, kPartThreads, 0, s>>>(
+          src, q, n, recv, m, level, pbits, bin_rank, nranks, off, ntiles, o, *peers);
+      ++h->launches;
+    }
+    return cuda_status(h, "part_pack_peer");
+  }
+  int64_t* hp = (int64_t*)h->pinned;
+  for (int sl = 0; sl < nslots; ++sl)
+    cudaMemcpyAsync(hp + sl, off + (int64_t)sl * ntiles, 8, cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status(h, "part_counts");
+  for (int sl = 0; sl < nslots; ++sl)
+    counts[sl] = (sl + 1 < nslots ? hp[sl + 1] : sr.total) - hp[sl];
+  return cuda_status(h, "part_counts");
+}
+
+extern "C" fmmb_status fmmb_part_counts(fmmb_handle_t h, const double* src, int64_t n,
+                                        const double* recv, int64_t m, int level, int pbits,
+                                        const uint32_t* bin_rank, int nranks, int64_t* counts,
+                                        void* stream) {
+  if (!counts) return FMMB_ERR_ARG;
+  return part_pass(h, src, nullptr, n, recv, m, level, pbits, bin_rank, nranks, 0, 0, nullptr,
+                   counts, (cudaStream_t)stream);
+}
+
+extern "C" fmmb_status fmmb_part_pack_peer(fmmb_handle_t h, const double* src, const double* q,
+                                           int64_t n, const double* recv, int64_t m, int level,
+                                           int pbits, const uint32_t* bin_rank, int nranks,
+                                           int64_t gbase_src, int64_t gbase_recv,
+                                           double* const* sxyz, double* const* sq,
+                                           int64_t* const* sgid, double* const* rxyz,
+                                           int64_t* const* rgid, const int64_t* soff,
+                                           const int64_t* roff, void* stream) {
+  using namespace fmmb;
+  if (!h || !sxyz || !sgid || !rxyz || !rgid || !soff || !roff) return FMMB_ERR_ARG;
+  if (nranks < 1 || nranks > kPartMaxRanks)
+    return fmmb_fail(h, FMMB_ERR_ARG, "nranks %d outside [1, %d]", nranks, kPartMaxRanks);
+  PeerOut po{};
+  for (int d = 0; d < nranks; ++d) {
+    po.sxyz[d] = sxyz[d];
+    po.sq[d] = sq ? sq[d] : nullptr;
+    po.sgid[d] = sgid[d];
+    po.rxyz[d] = rxyz[d];
+    po.rgid[d] = rgid[d];
+    po.soff[d] = soff[d];
+    po.roff[d] = roff[d];
+  }
+  return part_pass(h, src, q, n, recv, m, level, pbits, bin_rank, nranks, gbase_src, gbase_recv,
+                   &po, nullptr, (cudaStream_t)stream);
 }
 
 extern "C" fmmb_status fmmb_dist_sort(fmmb_handle_t h, const double* src, const double* q,

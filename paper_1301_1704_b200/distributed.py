@@ -35,6 +35,7 @@ partitioned path on a single GPU).  The per-rank device steps go through an
 from __future__ import annotations
 
 import ctypes as C
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -79,6 +80,17 @@ class Comm:
         """out[i] = [x of rank 0, ..., x of rank size-1] (same shapes)."""
         raise NotImplementedError
 
+    def peer_tables(self, bufs: list) -> list:
+        """Fused pack + exchange: bufs[i] = {name: device tensor} of driven
+        rank i's receive arrays.  Returns tables[i][name] = [device pointer
+        of rank d's array, usable from rank ranks[i]'s device, for d in
+        range(size)] (CUDA IPC across processes; P2P / same device in one)."""
+        raise NotImplementedError
+
+    def peer_barrier(self) -> None:
+        """Every rank's peer stores are complete and visible."""
+        raise NotImplementedError
+
 
 class SimComm(Comm):
     """All `size` ranks in this process (their tensors may share a device)."""
@@ -103,6 +115,15 @@ class SimComm(Comm):
 
     def all_gather(self, xs):
         return [list(xs) for _ in xs]
+
+    def peer_tables(self, bufs):
+        tab = {k: [b[k].data_ptr() if b[k] is not None and b[k].numel() else 0 for b in bufs]
+               for k in bufs[0]}
+        return [tab for _ in bufs]
+
+    def peer_barrier(self):
+        for d in range(torch.cuda.device_count()):
+            torch.cuda.synchronize(d)
 
 
 class TorchComm(Comm):
@@ -156,6 +177,36 @@ class TorchComm(Comm):
             out.append(recv[at: at + r * width].reshape((r,) + tail))
             at += r * width
         return [out]
+
+    def peer_tables(self, bufs):
+        """CUDA IPC: every rank shares its receive arrays' storages, opens the
+        others' (torch's own IPC path, lazily enabled peer access)."""
+        (b,) = bufs
+        mine = {k: (v.untyped_storage()._share_cuda_(), v.storage_offset() * v.element_size())
+                if v is not None and v.numel() else None for k, v in b.items()}
+        allm = [None] * self.size
+        self.dist.all_gather_object(allm, mine, group=self.group)
+        me = self.ranks[0]
+        self._peer_keep = []
+        tab = {}
+        for k in b:
+            ptrs = []
+            for d, md in enumerate(allm):
+                if md[k] is None:
+                    ptrs.append(0)
+                elif d == me:
+                    ptrs.append(b[k].data_ptr())
+                else:
+                    meta, off = md[k]
+                    st = torch.UntypedStorage._new_shared_cuda(*meta)
+                    self._peer_keep.append(st)
+                    ptrs.append(st.data_ptr() + off)
+            tab[k] = ptrs
+        return [tab]
+
+    def peer_barrier(self):
+        torch.cuda.synchronize()
+        self.dist.barrier(group=self.group)
 
     def all_gather(self, xs):
         (x,) = xs
@@ -217,6 +268,36 @@ class DeviceOps:
         self._count(h)
         c = list(counts)
         return sxyz, sq, sgid, rxyz, rgid, c[:nranks], c[nranks:]
+
+    def part_counts(self, src, recv, level, pbits, bin_rank, nranks):
+        dev = _lib.device_of(src.device)
+        h = _lib.handle(dev)
+        n, m = int(src.shape[0]), int(recv.shape[0])
+        counts = (C.c_int64 * (2 * nranks))()
+        br = bin_rank.to(device=dev, dtype=torch.int32).contiguous()
+        p = lambda t: t.data_ptr() if (t is not None and t.numel()) else None  # noqa: E731
+        st = _lib.load().fmmb_part_counts(h, p(src), n, p(recv), m, level, pbits, br.data_ptr(),
+                                          nranks, counts, _lib.stream_of(dev))
+        _lib.check(st, h)
+        self._count(h)
+        return list(counts)
+
+    def part_pack_peer(self, src, q, recv, level, pbits, bin_rank, nranks, gbase_src,
+                       gbase_recv, table, soff, roff):
+        dev = _lib.device_of(src.device)
+        h = _lib.handle(dev)
+        n, m = int(src.shape[0]), int(recv.shape[0])
+        br = bin_rank.to(device=dev, dtype=torch.int32).contiguous()
+        p = lambda t: t.data_ptr() if (t is not None and t.numel()) else None  # noqa: E731
+        P = C.c_void_p * nranks
+        arr = {k: P(*[v or None for v in table[k]]) for k in ("sxyz", "sq", "sgid", "rxyz", "rgid")}
+        st = _lib.load().fmmb_part_pack_peer(
+            h, p(src), p(q), n, p(recv), m, level, pbits, br.data_ptr(), nranks, gbase_src,
+            gbase_recv, arr["sxyz"], arr["sq"] if q is not None else None, arr["sgid"],
+            arr["rxyz"], arr["rgid"], (C.c_int64 * nranks)(*soff), (C.c_int64 * nranks)(*roff),
+            _lib.stream_of(dev))
+        _lib.check(st, h)
+        self._count(h)
 
     def dist_sort(self, src, q, sgid, recv, rgid, level):
         dev = _lib.device_of(src.device)
@@ -368,7 +449,7 @@ def _shard_csr(bm: torch.Tensor, offset: int, last: bool) -> torch.Tensor:
 
 
 def build_all_distributed(shards: list, max_level: int, comm: Comm, ops=None,
-                          pbits: int | None = None) -> list:
+                          pbits: int | None = None, exchange: str | None = None) -> list:
     """Partitioned build.  `shards[i] = (src, charges, recv)` of the rank
     comm.ranks[i]: device tensors, index-contiguous pieces of the global
     arrays in rank order.  Returns one DistShard per driven rank."""
@@ -394,6 +475,10 @@ def build_all_distributed(shards: list, max_level: int, comm: Comm, ops=None,
     hists = comm.allreduce_sum(hists)
     bin_rank = cut_bins(hists[0], P)
     windows = key_windows(bin_rank, P, L, pb)
+    exchange = exchange or os.environ.get("FMMB_DIST_EXCHANGE", "a2a")
+    if exchange == "peer":  # 3'. fused pack + exchange over peer memory
+        return _finish(shards, L, comm, ops, P, dev, gb, windows,
+                       _exchange_peer(shards, L, comm, ops, P, pb, bin_rank, gb, dev))
     # 3. pack + exchange
     packs = [ops.part_pack(s[0], s[1], s[2], L, pb, bin_rank, P, gb[i][0], gb[i][1])
              for i, s in enumerate(shards)]
@@ -418,22 +503,65 @@ def build_all_distributed(shards: list, max_level: int, comm: Comm, ops=None,
         ex[key] = comm.all_to_all([split(pk[idx], pk[cidx]) for pk in packs], rr)
     if with_q:
         ex["sq"] = comm.all_to_all([split(pk[1], pk[5]) for pk in packs], rsrc)
+    received = []
+    for i, r in enumerate(comm.ranks):
+        sent = sum(int(t.shape[0]) for d, t in enumerate(split(packs[i][0], packs[i][5])) if d != r)
+        sent_r = sum(int(t.shape[0]) for d, t in enumerate(split(packs[i][3], packs[i][6])) if d != r)
+        received.append({"sxyz": _cat(ex["sxyz"][i]), "sgid": _cat(ex["sgid"][i]),
+                         "rxyz": _cat(ex["rxyz"][i]), "rgid": _cat(ex["rgid"][i]),
+                         "sq": _cat(ex["sq"][i]) if with_q else None,
+                         "sent_points": sent + sent_r})
+    return _finish(shards, L, comm, ops, P, dev, gb, windows, received)
+
+
+def _exchange_peer(shards, L, comm, ops, P, pb, bin_rank, gb, dev) -> list:
+    """Fused pack + exchange: counts, one all-gather of them, receive arrays
+    sized and shared, then every rank stores its points straight into the
+    destinations' arrays (fmmb_part_pack_peer) -- no send buffers, no
+    separate all-to-all.  Receive order = (source rank, input index), as
+    with the all-to-all."""
+    with_q = shards[0][1] is not None
+    cnts = [ops.part_counts(s[0], s[2], L, pb, bin_rank, P) for s in shards]
+    allc = comm.all_gather([torch.tensor(c, dtype=torch.int64, device=dev[i])
+                            for i, c in enumerate(cnts)])
+    bufs, offs, received = [], [], []
+    for i, r in enumerate(comm.ranks):
+        mat = torch.stack([t.cpu() for t in allc[i]]).tolist()  # mat[s] = counts of rank s
+        n_in = sum(mat[s][r] for s in range(P))
+        m_in = sum(mat[s][P + r] for s in range(P))
+        soff = [sum(mat[s][d] for s in range(r)) for d in range(P)]
+        roff = [sum(mat[s][P + d] for s in range(r)) for d in range(P)]
+        f64, i64 = dict(dtype=torch.float64, device=dev[i]), dict(dtype=torch.int64, device=dev[i])
+        bufs.append({"sxyz": torch.empty((n_in, 3), **f64),
+                     "sq": torch.empty(n_in, **f64) if with_q else None,
+                     "sgid": torch.empty(n_in, **i64), "rxyz": torch.empty((m_in, 3), **f64),
+                     "rgid": torch.empty(m_in, **i64)})
+        offs.append((soff, roff))
+        c = cnts[i]
+        received.append({"sent_points": sum(c[d] + c[P + d] for d in range(P) if d != r)})
+    tables = comm.peer_tables(bufs)
+    for i, s in enumerate(shards):
+        ops.part_pack_peer(s[0], s[1], s[2], L, pb, bin_rank, P, gb[i][0], gb[i][1], tables[i],
+                           *offs[i])
+    comm.peer_barrier()
+    for i in range(len(shards)):
+        received[i].update(bufs[i])
+    return received
+
+
+def _finish(shards, L, comm, ops, P, dev, gb, windows, received) -> list:
+    """Local sort, global occupancy, owned lists, global offsets (steps 4-7)."""
+    nd = len(comm.ranks)
     results = []
     sorted_sets = []
     bmps = []
     for i, r in enumerate(comm.ranks):
-        src = _cat(ex["sxyz"][i])
-        sgid = _cat(ex["sgid"][i])
-        rxyz = _cat(ex["rxyz"][i])
-        rgid = _cat(ex["rgid"][i])
-        q = _cat(ex["sq"][i]) if with_q else None
-        sent = sum(int(t.shape[0]) for d, t in enumerate(split(packs[i][0], packs[i][5])) if d != r)
-        sent_r = sum(int(t.shape[0]) for d, t in enumerate(split(packs[i][3], packs[i][6])) if d != r)
+        rv = received[i]
         # 4. local sort phase
-        ss, sr, bmp = ops.dist_sort(src, q, sgid, rxyz, rgid, L)
+        ss, sr, bmp = ops.dist_sort(rv["sxyz"], rv["sq"], rv["sgid"], rv["rxyz"], rv["rgid"], L)
         sorted_sets.append((ss, sr))
         bmps.append(bmp)
-        results.append({"sent_points": sent + sent_r})
+        results.append({"sent_points": rv["sent_points"]})
     # 5. global occupancy
     gbmps = comm.allreduce_sum(bmps)
     # 6. owned lists

@@ -26,7 +26,10 @@ def _shards(arr, p):
     (2, 5000, 0, 3, "uniform", True),
     (3, 0, 4000, 3, "uniform", True),
 ])
-def test_partitioned_build_matches_single(gpu, p, n, m, level, dist, charges):
+@pytest.mark.parametrize("exchange", ["a2a", "peer"])
+def test_partitioned_build_matches_single(gpu, p, n, m, level, dist, charges, exchange):
+    """a2a: pack into send buffers + all-to-all; peer: the fused pack that
+    stores every point straight into its destination rank's arrays."""
     from paper_1301_1704_b200 import distributed as D
 
     src, q, _ = generate(n, 1, dist, 17)
@@ -38,7 +41,7 @@ def test_partitioned_build_matches_single(gpu, p, n, m, level, dist, charges):
     shards = [(t(s), t(qq) if q is not None else None, t(r)) for s, qq, r in
               zip(_shards(src, p), _shards(q if q is not None else np.zeros(n), p),
                   _shards(recv, p))]
-    out = D.build_all_distributed(shards, level, D.SimComm(p))
+    out = D.build_all_distributed(shards, level, D.SimComm(p), exchange=exchange)
     got = D.concat_shards(out)
     want = gpu.build_all(t(src), t(q) if q is not None else None, t(recv), max_level=level)
     errors = compare_structures(got.to_numpy(), want.to_numpy())

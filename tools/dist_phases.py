@@ -42,9 +42,11 @@ def timed(name, fn):
 
 comm = D.TorchComm()
 ops = D.DeviceOps()
-for n in ("allreduce_sum", "all_to_all", "all_gather"):
+for n in ("allreduce_sum", "all_to_all", "all_gather", "exchange_counts", "peer_tables",
+          "peer_barrier"):
     setattr(comm, n, timed("comm." + n, getattr(comm, n)))
-for n in ("part_histogram", "part_pack", "dist_sort", "dist_lists"):
+for n in ("part_histogram", "part_pack", "dist_sort", "dist_lists", "part_counts",
+          "part_pack_peer"):
     setattr(ops, n, timed("ops." + n, getattr(ops, n)))
 L = choose_max_level(wl.n * ws, 16)
 src, q, recv = generate(wl.n, wl.n, wl.dist, wl.seed + rank)
