@@ -63,3 +63,21 @@ def test_partition_is_balanced_and_contiguous(gpu):
     wins = [o.key_window for o in out]
     assert wins[0][0] == 0 and wins[-1][1] == 8**6
     assert all(wins[i][1] == wins[i + 1][0] for i in range(3))
+
+
+def test_peer_exchange_two_processes_over_ipc(gpu):
+    """Two ranks in two processes sharing the GPU: the fused pack stores into
+    the other process's receive arrays through CUDA IPC; the concatenated
+    shards equal the single-GPU build for both exchanges."""
+    import os
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    out = subprocess.run(
+        [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+         "--master-addr", "127.0.0.1", "--master-port", "29657",
+         os.path.join(root, "tools", "peer_ipc_check.py")],
+        cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    assert "peer OK" in out.stdout and "a2a OK" in out.stdout
