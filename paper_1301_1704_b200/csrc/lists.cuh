@@ -208,6 +208,175 @@ __device__ __forceinline__ uint64_t popc_bytes(uint64_t x) {
   return (x + (x >> 4)) & 0x0F0F0F0F0F0F0F0Full;
 }
 
+// Write pass.  Lanes hold the window neighbours sorted by Morton key; the
+// 27x8 candidate children of a row are visited in output order as 7 chunks
+// of 32 (lane = candidate: slot = 4*chunk + lane/8, child c = lane%8).  Every
+// row-independent quantity of a chunk (occupancy, rank, code base, the near
+// bit for each of the 8 child receivers) is computed once per P; a row is
+// then one ballot-compaction per chunk with coalesced stores straight to HBM.
+// The rows of P's child receivers are consecutive, so one bookmark read per P.
+__device__ __forceinline__ unsigned ballot_full(unsigned pred) {
+  unsigned b;
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
+               "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t}" : "=r"(b) : "r"(pred));
+  return b;
+}
+
+// predicated stores (no branch around them)
+__device__ __forceinline__ void st_rank_code(unsigned pred, int64_t* r, int64_t rank, int16_t* c,
+                                             int code) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
+      "@p st.global.s64 [%1], %2;\n\t@p st.global.s16 [%3], %4;\n\t}" ::"r"(pred),
+      "l"(r), "l"(rank), "l"(c), "h"((short)code)
+      : "memory");
+}
+__device__ __forceinline__ void st_rank(unsigned pred, int64_t* r, int64_t rank) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.global.s64 [%1], %2;\n\t}" ::
+                   "r"(pred), "l"(r), "l"(rank)
+               : "memory");
+}
+
+template <bool E4, bool E2>
+__device__ __forceinline__ void write_rows(uint32_t rm, const uint32_t (&meta)[7],
+                                           const uint32_t (&rank)[7], int64_t* __restrict__ r4,
+                                           int16_t* __restrict__ c4, int64_t* __restrict__ r2) {
+  const unsigned lt = lanemask_lt();
+  uint32_t rbits = rm;
+  while (rbits) {
+    const int cr = __ffs(rbits) - 1;
+    rbits &= rbits - 1;
+    const int crw = (cr & 1) + 7 * ((cr >> 1) & 1) + 49 * ((cr >> 2) & 1);
+    const int sh = 1 + cr;
+#pragma unroll
+    for (int ch = 0; ch < 7; ++ch) {
+      const uint32_t m = meta[ch];
+      const uint32_t nb = m >> sh;
+      if (E4) {
+        const unsigned v = m & ~nb & 1u;
+        const unsigned b = ballot_full(v);
+        const unsigned at = __popc(b & lt);
+        st_rank_code(v, r4 + at, (int64_t)rank[ch], c4 + at, (int)(m >> 9) - crw);
+        r4 += __popc(b);
+        c4 += __popc(b);
+      }
+      if (E2) {
+        const unsigned v = m & nb & 1u;
+        const unsigned b = ballot_full(v);
+        st_rank(v, r2 + __popc(b & lt), (int64_t)rank[ch]);
+        r2 += __popc(b);
+      }
+    }
+  }
+}
+
+// One receiver parent P (level l-1, rank j among the work parents of level
+// l): its rows of E4 (and E2 at l == L).  FRESH: the bookmarks were written
+// by this kernel (read through L2, not the read-only path).
+template <bool FRESH>
+__device__ __forceinline__ void write_parent(const ListsParams& p, const ListsLayout& lay,
+                                             int L, int l, int64_t j, int lane) {
+  const unsigned FULL = 0xffffffffu;
+  const int c = lane & 7;
+  // code contribution of the candidate child c: (c_x + 7 c_y + 49 c_z) + 3*57
+  const int cc = (c & 1) + 7 * ((c >> 1) & 1) + 49 * ((c >> 2) & 1) + 171;
+  const uint64_t P = __ldg(p.rkeys[l - 1] + lay.p_lo[l] + j);
+  uint64_t qk = window_key(P, l, lane);
+  int o = lane;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int d = k >> 1; d > 0; d >>= 1) {
+      const uint64_t ok = __shfl_xor_sync(FULL, qk, d);
+      const int oo = __shfl_xor_sync(FULL, o, d);
+      const bool want_min = ((lane & d) == 0) == ((lane & k) == 0);
+      if (want_min ? (ok < qk) : (ok > qk)) {
+        qk = ok;
+        o = oo;
+      }
+    }
+  }
+  uint32_t sm = 0, sfirst = 0;
+  if (qk != ~0ull)
+    children_of(p.bmp + p.bmp_off[0][l], p.dir + p.bmp_off[0][l], qk, sm, sfirst);
+  uint32_t rm, rfirst;
+  children_of(p.bmp + p.bmp_off[1][l], p.dir + p.bmp_off[1][l], P, rm, rfirst);
+  // per chunk: meta = occ | near-over-cr (8 bits) << 1 | code base << 9
+  const uint32_t slot_word = sm | ((uint32_t)(o < 27 ? o : 13) << 8);
+  uint32_t meta[7], rank[7];
+#pragma unroll
+  for (int ch = 0; ch < 7; ++ch) {
+    const int slot = 4 * ch + (lane >> 3);
+    const uint32_t v = __shfl_sync(FULL, slot_word, slot);
+    const uint32_t f = __shfl_sync(FULL, sfirst, slot);
+    const uint32_t smk = v & 0xFFu;
+    const int so = (int)(v >> 8);
+    const uint64_t nw = kNear.w[so];
+    uint32_t nearcr = 0;
+#pragma unroll
+    for (int cr = 0; cr < 8; ++cr) nearcr |= ((uint32_t)(nw >> (8 * cr + c)) & 1u) << cr;
+    const int sx = so % 3 - 1, sy = (so / 3) % 3 - 1, sz = so / 9 - 1;
+    const uint32_t code0 = (uint32_t)(2 * sx + 7 * 2 * sy + 49 * 2 * sz + cc);
+    const bool occ = slot < 27 && ((smk >> c) & 1u);
+    meta[ch] = (occ ? 1u : 0u) | (nearcr << 1) | (code0 << 9);
+    rank[ch] = f + __popc(smk & ((1u << c) - 1u));
+  }
+  int64_t* r4 = p.ranks_out[l];
+  int16_t* c4 = p.codes_out[l];
+  int64_t* r2 = p.ranks_out[0];
+  // owned children (a contiguous run of ranks) and the first one's CSR row
+  uint32_t own = 0;
+  int64_t r0 = -1;
+  {
+    int64_t r = rfirst;
+#pragma unroll
+    for (int c = 0; c < 8; ++c)
+      if ((rm >> c) & 1u) {
+        if (r >= lay.r_lo[l] && r < lay.r_hi[l]) {
+          own |= 1u << c;
+          if (r0 < 0) r0 = r - lay.r_lo[l];
+        }
+        ++r;
+      }
+  }
+  rm = own;
+  if (!rm) return;
+  rfirst = (uint32_t)r0;
+  if (l == L) {
+    const int64_t w2 = FRESH ? __ldcg(p.bm[0] + rfirst) : __ldg(p.bm[0] + rfirst);
+    if (l >= 2) {
+      const int64_t w4 = FRESH ? __ldcg(p.bm[l] + rfirst) : __ldg(p.bm[l] + rfirst);
+      write_rows<true, true>(rm, meta, rank, r4 + w4, c4 + w4, r2 + w2);
+    } else {
+      write_rows<false, true>(rm, meta, rank, nullptr, nullptr, r2 + w2);
+    }
+  } else {
+    const int64_t w4 = FRESH ? __ldcg(p.bm[l] + rfirst) : __ldg(p.bm[l] + rfirst);
+    write_rows<true, false>(rm, meta, rank, r4 + w4, c4 + w4, nullptr);
+  }
+}
+
+__global__ void __launch_bounds__(kLThreads)
+    k_lists_write(const __grid_constant__ ListsParams p, const ListsLayout* __restrict__ glay) {
+  __shared__ ListsLayout lay;
+  load_layout(glay, lay);
+  __syncthreads();
+  const int L = p.level;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nwork = lay.work_off[L + 1];
+  const int64_t gstride = (int64_t)gridDim.x * kLWarps;
+  for (int64_t gw = (int64_t)blockIdx.x * kLWarps + warp; gw < nwork; gw += gstride) {
+    int l = lay.lmin;
+    while (lay.work_off[l + 1] <= gw) ++l;
+    const int64_t j = gw - lay.work_off[l];
+    if (l == 0) {
+      if (lane == 0 && p.ktot[0]) p.ranks_out[0][p.bm[0][0]] = 0;
+      continue;
+    }
+    write_parent<false>(p, lay, L, l, j, lane);
+  }
+}
+
 // Count + CSR scan in one pass.  A tile is kCsParents consecutive receiver
 // parents P of one level (8 per warp); for each child receiver r of P it
 // counts |E4_l(r)| (and |E2(r)| at l == L) -- lane = window slot, the
@@ -216,6 +385,7 @@ __device__ __forceinline__ uint64_t popc_bytes(uint64_t x) {
 // receiver keys) are scanned in shared memory and offset by a decoupled
 // look-back over the level's tiles (tickets keep tiles in order).  Writes
 // the bookmark arrays and the per-level totals.
+template <bool WRITE>
 __global__ void __launch_bounds__(kLThreads)
     k_lists_cscan(const __grid_constant__ ListsParams p, const ListsLayout* __restrict__ glay,
                   uint64_t* __restrict__ st4, uint64_t* __restrict__ st2,
@@ -347,164 +517,11 @@ __global__ void __launch_bounds__(kLThreads)
       seg_totals[0] = base2 + tot2;
     }
   }
-}
-
-// Write pass.  Lanes hold the window neighbours sorted by Morton key; the
-// 27x8 candidate children of a row are visited in output order as 7 chunks
-// of 32 (lane = candidate: slot = 4*chunk + lane/8, child c = lane%8).  Every
-// row-independent quantity of a chunk (occupancy, rank, code base, the near
-// bit for each of the 8 child receivers) is computed once per P; a row is
-// then one ballot-compaction per chunk with coalesced stores straight to HBM.
-// The rows of P's child receivers are consecutive, so one bookmark read per P.
-__device__ __forceinline__ unsigned ballot_full(unsigned pred) {
-  unsigned b;
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %1, 0;\n\t"
-               "vote.sync.ballot.b32 %0, p, 0xffffffff;\n\t}" : "=r"(b) : "r"(pred));
-  return b;
-}
-
-// predicated stores (no branch around them)
-__device__ __forceinline__ void st_rank_code(unsigned pred, int64_t* r, int64_t rank, int16_t* c,
-                                             int code) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t"
-      "@p st.global.s64 [%1], %2;\n\t@p st.global.s16 [%3], %4;\n\t}" ::"r"(pred),
-      "l"(r), "l"(rank), "l"(c), "h"((short)code)
-      : "memory");
-}
-__device__ __forceinline__ void st_rank(unsigned pred, int64_t* r, int64_t rank) {
-  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.global.s64 [%1], %2;\n\t}" ::
-                   "r"(pred), "l"(r), "l"(rank)
-               : "memory");
-}
-
-template <bool E4, bool E2>
-__device__ __forceinline__ void write_rows(uint32_t rm, const uint32_t (&meta)[7],
-                                           const uint32_t (&rank)[7], int64_t* __restrict__ r4,
-                                           int16_t* __restrict__ c4, int64_t* __restrict__ r2) {
-  const unsigned lt = lanemask_lt();
-  uint32_t rbits = rm;
-  while (rbits) {
-    const int cr = __ffs(rbits) - 1;
-    rbits &= rbits - 1;
-    const int crw = (cr & 1) + 7 * ((cr >> 1) & 1) + 49 * ((cr >> 2) & 1);
-    const int sh = 1 + cr;
-#pragma unroll
-    for (int ch = 0; ch < 7; ++ch) {
-      const uint32_t m = meta[ch];
-      const uint32_t nb = m >> sh;
-      if (E4) {
-        const unsigned v = m & ~nb & 1u;
-        const unsigned b = ballot_full(v);
-        const unsigned at = __popc(b & lt);
-        st_rank_code(v, r4 + at, (int64_t)rank[ch], c4 + at, (int)(m >> 9) - crw);
-        r4 += __popc(b);
-        c4 += __popc(b);
-      }
-      if (E2) {
-        const unsigned v = m & nb & 1u;
-        const unsigned b = ballot_full(v);
-        st_rank(v, r2 + __popc(b & lt), (int64_t)rank[ch]);
-        r2 += __popc(b);
-      }
-    }
-  }
-}
-
-__global__ void __launch_bounds__(kLThreads)
-    k_lists_write(const __grid_constant__ ListsParams p, const ListsLayout* __restrict__ glay) {
-  __shared__ ListsLayout lay;
-  load_layout(glay, lay);
-  __syncthreads();
-  const int L = p.level;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t nwork = lay.work_off[L + 1];
-  const int64_t gstride = (int64_t)gridDim.x * kLWarps;
-  const unsigned FULL = 0xffffffffu;
-  const int c = lane & 7;
-  // code contribution of the candidate child c: (c_x + 7 c_y + 49 c_z) + 3*57
-  const int cc = (c & 1) + 7 * ((c >> 1) & 1) + 49 * ((c >> 2) & 1) + 171;
-  for (int64_t gw = (int64_t)blockIdx.x * kLWarps + warp; gw < nwork; gw += gstride) {
-    int l = lay.lmin;
-    while (lay.work_off[l + 1] <= gw) ++l;
-    const int64_t j = gw - lay.work_off[l];
-    if (l == 0) {
-      if (lane == 0 && p.ktot[0]) p.ranks_out[0][p.bm[0][0]] = 0;
-      continue;
-    }
-    const uint64_t P = __ldg(p.rkeys[l - 1] + lay.p_lo[l] + j);
-    uint64_t qk = window_key(P, l, lane);
-    int o = lane;
-#pragma unroll
-    for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-      for (int d = k >> 1; d > 0; d >>= 1) {
-        const uint64_t ok = __shfl_xor_sync(FULL, qk, d);
-        const int oo = __shfl_xor_sync(FULL, o, d);
-        const bool want_min = ((lane & d) == 0) == ((lane & k) == 0);
-        if (want_min ? (ok < qk) : (ok > qk)) {
-          qk = ok;
-          o = oo;
-        }
-      }
-    }
-    uint32_t sm = 0, sfirst = 0;
-    if (qk != ~0ull)
-      children_of(p.bmp + p.bmp_off[0][l], p.dir + p.bmp_off[0][l], qk, sm, sfirst);
-    uint32_t rm, rfirst;
-    children_of(p.bmp + p.bmp_off[1][l], p.dir + p.bmp_off[1][l], P, rm, rfirst);
-    // per chunk: meta = occ | near-over-cr (8 bits) << 1 | code base << 9
-    const uint32_t slot_word = sm | ((uint32_t)(o < 27 ? o : 13) << 8);
-    uint32_t meta[7], rank[7];
-#pragma unroll
-    for (int ch = 0; ch < 7; ++ch) {
-      const int slot = 4 * ch + (lane >> 3);
-      const uint32_t v = __shfl_sync(FULL, slot_word, slot);
-      const uint32_t f = __shfl_sync(FULL, sfirst, slot);
-      const uint32_t smk = v & 0xFFu;
-      const int so = (int)(v >> 8);
-      const uint64_t nw = kNear.w[so];
-      uint32_t nearcr = 0;
-#pragma unroll
-      for (int cr = 0; cr < 8; ++cr) nearcr |= ((uint32_t)(nw >> (8 * cr + c)) & 1u) << cr;
-      const int sx = so % 3 - 1, sy = (so / 3) % 3 - 1, sz = so / 9 - 1;
-      const uint32_t code0 = (uint32_t)(2 * sx + 7 * 2 * sy + 49 * 2 * sz + cc);
-      const bool occ = slot < 27 && ((smk >> c) & 1u);
-      meta[ch] = (occ ? 1u : 0u) | (nearcr << 1) | (code0 << 9);
-      rank[ch] = f + __popc(smk & ((1u << c) - 1u));
-    }
-    int64_t* r4 = p.ranks_out[l];
-    int16_t* c4 = p.codes_out[l];
-    int64_t* r2 = p.ranks_out[0];
-    // owned children (a contiguous run of ranks) and the first one's CSR row
-    uint32_t own = 0;
-    int64_t r0 = -1;
-    {
-      int64_t r = rfirst;
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-        if ((rm >> c) & 1u) {
-          if (r >= lay.r_lo[l] && r < lay.r_hi[l]) {
-            own |= 1u << c;
-            if (r0 < 0) r0 = r - lay.r_lo[l];
-          }
-          ++r;
-        }
-    }
-    rm = own;
-    if (!rm) continue;
-    rfirst = (uint32_t)r0;
-    if (l == L) {
-      const int64_t w2 = __ldg(p.bm[0] + rfirst);
-      if (l >= 2) {
-        const int64_t w4 = __ldg(p.bm[l] + rfirst);
-        write_rows<true, true>(rm, meta, rank, r4 + w4, c4 + w4, r2 + w2);
-      } else {
-        write_rows<false, true>(rm, meta, rank, nullptr, nullptr, r2 + w2);
-      }
-    } else {
-      const int64_t w4 = __ldg(p.bm[l] + rfirst);
-      write_rows<true, false>(rm, meta, rank, r4 + w4, c4 + w4, nullptr);
+  if (WRITE) {  // fused write: this tile's rows, offsets from the bookmarks just written
+    __syncthreads();
+    for (int k = 0; k < kPW; ++k) {
+      const int64_t j = j0 + warp * kPW + k;
+      if (j < np) write_parent<true>(p, lay, L, l, j, lane);
     }
   }
 }
