@@ -48,8 +48,11 @@ def parse():
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--workload", default="c2", choices=["c1", "c2", "c3", "c4"])
+    p.add_argument("--workload", default=None, choices=["c1", "c2", "c3", "c4", "c5"],
+                   help="default: c2 on one GPU, c5 shards (2^27 + 2^27 per GPU, L=8) for N > 1")
     p.add_argument("--e2e-steps", type=int, default=3)
+    p.add_argument("--partitioned", action="store_true",
+                   help="run the Morton-range partitioned path even at one process (P = 1)")
     p.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-nf", action="store_true", help="skip the near-field consumer timing")
@@ -67,73 +70,100 @@ def dist_env():
 
 
 # --------------------------------------------------------- cpu reference
-CPU_SAMPLE = {"n": 2**21, "level": 6, "dist": "uniform", "seed": 1}
+def workload_inputs(name: str):
+    """The exact numpy inputs of a workload (the GPU arm uploads the same
+    arrays): c1-c3 from fmmkit.cli.generate's streams, c4 = one perturbed
+    rebuild step (workloads.c4_step_inputs, the c4 golden case)."""
+    from paper_1301_1704_b200.workloads import WORKLOADS, c4_step_inputs, generate
+
+    wl = WORKLOADS[name]
+    if name == "c4":
+        src, q, recv = c4_step_inputs(wl.n, wl.seed, 1)
+    else:
+        src, q, recv = generate(wl.n, wl.n, wl.dist, wl.seed)
+    return src, q, recv, wl.level
 
 
-def cpu_reference_rate(max_seconds: float = 25.0, steps: int | None = None, warmup: int = 0):
-    """Reference CPU build_all on a bounded sample of the workload: N=M=2^21
-    uniform at L=6 (8 points per finest box, the c2 occupancy).  Returns
-    (particles/s, kind, cores, sample, per-step rates)."""
-    from paper_1301_1704_b200.workloads import generate
-
-    src, q, recv = generate(CPU_SAMPLE["n"], CPU_SAMPLE["n"], CPU_SAMPLE["dist"],
-                            CPU_SAMPLE["seed"])
-    L = CPU_SAMPLE["level"]
+def reference_build_fn():
+    """(build_all callable, kind): the unmodified reference compiled from its
+    sources into oracle/_ref (fmmkit, compiled backend, deterministic mode),
+    else the C restatement of the same algorithm (oracle/)."""
     ref_dir = os.path.join(ROOT, "oracle", "_ref")
-    kind = "reference"
     try:
         sys.path.insert(0, ref_dir)
         import fmmkit  # noqa: F401  (oracle/_ref: the unmodified reference)
 
         assert fmmkit.backend_name() == "compiled"
-        run = lambda: fmmkit.build_all(src, q, recv, max_level=L)  # noqa: E731
-    except Exception:  # the C restatement of the same algorithm
+        return (lambda s, q, r, L: fmmkit.build_all(s, q, r, max_level=L)), "reference"
+    except Exception:
         sys.path.pop(0)
         from oracle import oracle as orc
 
-        kind = "port"
-        run = lambda: orc.build_all(src, q, recv, L)  # noqa: E731
-    for _ in range(warmup):  # untimed
-        run()
-    rates = []
-    t_start = time.perf_counter()
+        return (lambda s, q, r, L: orc.build_all(s, q, r, L)), "port"
+
+
+def cpu_reference_rate(workload: str, steps: int = 1, budget_s: float = 90.0, inputs=None):
+    """The reference CPU build_all on the IDENTICAL inputs of the workload
+    (BASELINE.md section 3): up to `steps` timed builds, stopping once
+    `budget_s` of build time is spent (at least one).  The deterministic
+    reference build is single-threaded, so cores = 1.
+    Returns (particles/s, kind, cores, sample, per-build seconds, last result)."""
+    src, q, recv, L = inputs if inputs is not None else workload_inputs(workload)
+    run, kind = reference_build_fn()
+    times = []
+    res = None
     while True:
+        res = None
         t0 = time.perf_counter()
-        run()
-        dt = time.perf_counter() - t0
-        rates.append(2 * CPU_SAMPLE["n"] / dt)
-        if steps is not None:
-            if len(rates) >= steps:
-                break
-        elif time.perf_counter() - t_start > max_seconds or len(rates) >= 5:
+        res = run(src, q, recv, L)
+        times.append(time.perf_counter() - t0)
+        if len(times) >= steps or sum(times) > budget_s:
             break
-    sample = (f"N=M=2^21 uniform, L=6 (c2 occupancy: 8 points per box), "
+    n_part = src.shape[0] + recv.shape[0]
+    med = statistics.median(times)
+    sample = (f"the full {workload} workload (identical arrays: N={src.shape[0]}, "
+              f"M={recv.shape[0]}, max_level={L}), "
               f"{'compiled fmmkit (oracle/_ref)' if kind == 'reference' else 'C oracle port'}, "
-              f"deterministic mode (single-threaded), median of {len(rates)} builds")
-    return statistics.median(rates), kind, 1, sample, rates
+              f"deterministic mode (single-threaded; os.cpu_count()={os.cpu_count()}), "
+              f"median of {len(times)} build(s)")
+    return n_part / med, kind, 1, sample, times, res
 
 
 def run_reference_arm(args):
     ws, rank, _ = dist_env()
     if rank != 0:
         return
-    # the deterministic reference build is single-threaded (SURVEY 8(d): no
-    # threading outside mode="atomic", whose within-box order differs)
-    wu = max(0, min(args.warmup, 3))
-    rate, kind, cores, sample, rates = cpu_reference_rate(steps=max(1, args.steps), warmup=wu)
-    dt = 2 * CPU_SAMPLE["n"] / rate
+    wl = "c2" if args.workload in ("c5",) else args.workload
+    # one c2 reference build takes ~30 s: time up to --steps builds within a
+    # ~2-minute budget (no warm-up: nothing to warm in a 30-s CPU build)
+    rate, kind, cores, sample, times, _ = cpu_reference_rate(wl, steps=max(1, args.steps),
+                                                             budget_s=100.0)
     line = {
         "impl": "reference", "metric": METRIC, "value": rate, "unit": UNIT,
-        "n_gpus": args.gpus, "steps": len(rates), "warmup": wu,
-        "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{args.workload} (bounded CPU sample)", "sample": sample},
+        "n_gpus": args.gpus, "steps": len(times), "warmup": 0,
+        "ms_per_step": statistics.median(times) * 1e3, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": workload_config(wl, 1),
         "cpu_baseline": {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
                          "sample": sample},
         "e2e": {"value": rate, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
+        "build_seconds": [round(t, 3) for t in times],
     }
     print(json.dumps(line), flush=True)
+
+
+def workload_config(name: str, ws: int) -> dict:
+    from paper_1301_1704_b200.workloads import WORKLOADS
+
+    wl = WORKLOADS[name]
+    extra = ", one perturbed rebuild step per timed step" if name == "c4" else ""
+    return {
+        "workload": f"{wl.name}: N=M={wl.n} {wl.dist}, max_level={wl.level}, seed={wl.seed}{extra}",
+        "global_batch_particles": 2 * wl.n * ws,
+        "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
+        "l2": "inputs larger than the 126 MB L2 (c2: 0.94 GB); no flush",
+    }
 
 
 # ------------------------------------------------------------------ clocks
@@ -186,49 +216,67 @@ class ClockSampler:
 
 
 # -------------------------------------------------------------- our arm
+def flat_outputs(st) -> dict:
+    """Every output array of an FmmStructures (numpy), keyed like the golden files."""
+    out = {}
+    for side, ps in (("src", st.sorted_src), ("recv", st.sorted_recv)):
+        for f in ("points", "charges", "permutation", "bookmarks", "non_empty_index", "boxes"):
+            v = getattr(ps, f)
+            if v is not None:
+                out[f"{side}.{f}"] = np.asarray(v)
+    out["neighbor_bookmark"] = np.asarray(st.neighbor_table.neighbor_bookmark)
+    out["neighbor_list"] = np.asarray(st.neighbor_table.neighbor_list)
+    for l, v in st.directory.src_boxes.items():
+        out[f"dir_src.{l}"] = np.asarray(v)
+    for l, v in st.directory.recv_boxes.items():
+        out[f"dir_recv.{l}"] = np.asarray(v)
+    for f in ("bookmark", "ranks", "codes"):
+        for l, v in getattr(st.stencils, f).items():
+            out[f"st_{f}.{l}"] = np.asarray(v)
+    return out
+
+
+def compare_outputs(got, want) -> dict:
+    """Bit-equality of every output array (values, dtypes, shapes)."""
+    g, w = flat_outputs(got), flat_outputs(want)
+    bad = sorted(k for k in set(g) | set(w)
+                 if k not in g or k not in w or g[k].dtype != w[k].dtype
+                 or g[k].shape != w[k].shape or not np.array_equal(g[k], w[k]))
+    return {"bit_exact": not bad, "arrays": len(w), "mismatched": bad[:8],
+            "bytes": int(sum(v.nbytes for v in w.values()))}
+
+
 def run_ours(args):
     import torch
 
     import paper_1301_1704_b200 as fb
     from paper_1301_1704_b200 import roofline
-    from paper_1301_1704_b200.workloads import WORKLOADS, generate, perturb
+    from paper_1301_1704_b200.workloads import perturb_device
 
-    ws, rank, local = dist_env()
-    dist = None
-    if ws > 1:
-        import torch.distributed as dist
-
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    else:
-        torch.cuda.set_device(0)
+    torch.cuda.set_device(0)
     dev = torch.device("cuda", torch.cuda.current_device())
     fb._lib.set_sort_path(args.sort_path, dev)
-    wl = WORKLOADS[args.workload]
-    src_np, q_np, recv_np = generate(wl.n, wl.n, wl.dist, wl.seed + rank)
+    src_np, q_np, recv_np, L = workload_inputs(args.workload)
     src = torch.from_numpy(src_np).to(dev)
     q = torch.from_numpy(q_np).to(dev)
     recv = torch.from_numpy(recv_np).to(dev)
-    L = wl.level
+    n_part = src.shape[0] + recv.shape[0]
     stream = torch.cuda.current_stream(dev)
-    rng = np.random.default_rng(123)
+    c4 = args.workload == "c4"
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(123)
 
     def step():
+        if c4:  # dynamic rebuild: the particles move, then the full rebuild
+            perturb_device(src, gen)
+            perturb_device(recv, gen)
         return fb.build_all_device(src, q, recv, L)
 
-    if args.workload == "c4":  # dynamic rebuild: fresh perturbed positions each step
-        pert = [(torch.from_numpy(perturb(src_np, rng)).to(dev),
-                 torch.from_numpy(perturb(recv_np, rng)).to(dev)) for _ in range(2)]
-
-    # warm-up (also sizes the caching allocator for the outputs); c4 warms up on
-    # the same alternating perturbed sets the timed steps rebuild
+    # warm-up (also sizes the caching allocator for the outputs)
     st = None
-    for k in range(max(args.warmup, 3)):
+    for _ in range(max(args.warmup, 3)):
         st = None
-        if args.workload == "c4":
-            st = fb.build_all_device(pert[k % 2][0], q, pert[k % 2][1], L)
-        else:
-            st = step()
+        st = step()
     counts = roofline.build_counts(st)
     balg = roofline.build_bytes(counts)
     wbytes = roofline.list_write_bytes(counts)
@@ -237,40 +285,27 @@ def run_ours(args):
 
     clocks = ClockSampler(dev.index)
     clocks.start()
-    if dist is not None:
-        dist.barrier()
     torch.cuda.synchronize()
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     phases = []
     launches = 0
     ev0.record(stream)
-    for k in range(args.steps):
-        if args.workload == "c4":
-            s_in, r_in = pert[k % 2]
-            st = fb.build_all_device(s_in, q, r_in, L)
-        else:
-            st = step()
+    for _ in range(args.steps):
+        st = step()
         phases.append(st.build_seconds)
-        launches += st.n_launches
+        launches += st.n_launches + (6 if c4 else 0)  # + randn/add/remainder x2 (torch)
         st = None
     ev1.record(stream)
     torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
     clk = clocks.stop()
     elapsed = ev0.elapsed_time(ev1) * 1e-3
-    if dist is not None:
-        t = torch.tensor([elapsed], device=dev, dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        elapsed = float(t.item())
-    units = 2 * wl.n * args.steps * ws
-    value = units / elapsed
+    value = n_part * args.steps / elapsed
     ms_step = elapsed / args.steps * 1e3
 
-    ph = {k: statistics.median([float(p[k]) for p in phases]) * 1e3
-          for k in ("sort_sources", "level_directory", "lists_count", "size_readback",
-                    "lists_write")}
+    keys = ("sort_sources", "level_directory", "lists_count", "size_readback", "lists_write")
+    ph = {k: statistics.median([float(p[k]) for p in phases]) * 1e3 for k in keys}
+    build_ms = statistics.median([sum(float(p[k]) for k in keys) for p in phases]) * 1e3
     peak, peak_src = roofline.measured_hbm_gbs(ROOT)
     traffic = None  # DRAM bytes per launch of the dominant kernel, from the committed ncu capture
     try:
@@ -286,7 +321,8 @@ def run_ours(args):
 
     # ---- end to end: pinned host inputs -> public API -> numpy outputs
     e2e = None
-    if not args.no_e2e and rank == 0:
+    ours_np = None
+    if not args.no_e2e:
         h_src = torch.from_numpy(src_np).pin_memory()
         h_q = torch.from_numpy(q_np).pin_memory()
         h_recv = torch.from_numpy(recv_np).pin_memory()
@@ -300,16 +336,17 @@ def run_ours(args):
             t0 = time.perf_counter()
             res = fb.build_all(h_src, h_q, h_recv, max_level=L)
             times.append(time.perf_counter() - t0)
+            ours_np = res
             res = None
-        e2e = {"value": 2 * wl.n / statistics.median(times), "unit": UNIT,
+        e2e = {"value": n_part / statistics.median(times), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "ms_per_step": statistics.median(times) * 1e3}
 
     # ---- the near-field pass consuming the device-built
     # structures in place (not part of the build metric; reported beside it)
     nf = None
-    if not args.no_nf and rank == 0 and args.workload != "c4":
-        st = step()
+    if not args.no_nf and not c4:
+        st = fb.build_all_device(src, q, recv, L)
         ss, sr, nt = st.sorted_src, st.sorted_recv, st.neighbor_table
         cs = torch.nn.functional.pad(torch.cumsum(torch.diff(ss.bookmarks)[nt.neighbor_list], 0),
                                      (1, 0))
@@ -330,46 +367,52 @@ def run_ours(args):
               "interactions_per_s": pairs / t_nf, "dtype": "f64 (bit-exact vs compiled reference)"}
         st = None
 
+    # ---- the reference CPU build on the identical arrays, and bit-equality
+    # of every output array with this run's end-to-end result
     cpu = None
-    if not args.no_cpu and rank == 0:
-        rate, kind, cores, sample, _ = cpu_reference_rate()
+    parity = None
+    if not args.no_cpu:
+        rate, kind, cores, sample, _, ref_res = cpu_reference_rate(
+            args.workload, steps=1, inputs=(src_np, q_np, recv_np, L))
         cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind, "sample": sample}
+        if ours_np is not None:
+            parity = compare_outputs(ours_np, ref_res) | {"against": kind}
+        ref_res = None
+    ours_np = None
 
-    if rank == 0:
-        line = {
-            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
-            "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64/u64 (integer keys, f64 points)",
-            "data": "synthetic (fmmkit.cli.generate Philox streams)",
-            "config": {
-                "workload": f"{wl.name}: N=M={wl.n} {wl.dist}, max_level={L}, seed={wl.seed}",
-                "global_batch_particles": 2 * wl.n * ws,
-                "parallelism": "single GPU" if ws == 1 else f"{ws} independent replicas",
-                "l2": "inputs (0.94 GB at c2) larger than the 126 MB L2; no flush",
-            },
-            "roofline": {
-                "bound": "hbm", "kernel": "k_lists_write (E2+E4 list write)",
-                "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                "peak_source": peak_src, "traffic": traffic,
-                "alg_bytes_per_launch": wbytes, "avg_launch_ms": ph["lists_write"],
-            },
-            "build_roofline": {
-                "alg_bytes_per_step": balg, "achieved_gbs": build_gbs,
-                "frac_of_measured": build_gbs / peak,
-                "frac_of_nominal_8tbs": build_gbs / roofline.NOMINAL_HBM_GBS,
-            },
-            "phases_ms": ph,
-            "counts": {k: counts[k] for k in ("ks", "kr", "e2")} | {
-                "stencil_entries": int(sum(counts["s_l"].values()))},
-            "clocks": clk,
-            "e2e": e2e,
-            "cpu_baseline": cpu,
-            "gpu_launches": int(launches),
-            "near_field": nf,
-        }
-        print(json.dumps(line), flush=True)
-    if dist is not None:
-        dist.destroy_process_group()
+    cfg = workload_config(args.workload, 1)
+    if c4:
+        cfg["step"] = ("device perturbation x <- remainder(x + N(0,1e-3), 1) of both sets "
+                       "(timed, torch ops) + full rebuild; trajectory seed 123")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64/u64 (integer keys, f64 points)",
+        "data": "synthetic (fmmkit.cli.generate Philox streams)",
+        "config": cfg,
+        "roofline": {
+            "bound": "hbm", "kernel": "k_lists_write (E2+E4 list write)",
+            "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+            "peak_source": peak_src, "traffic": traffic,
+            "alg_bytes_per_launch": wbytes, "avg_launch_ms": ph["lists_write"],
+        },
+        "build_roofline": {
+            "alg_bytes_per_step": balg, "achieved_gbs": build_gbs,
+            "frac_of_measured": build_gbs / peak,
+            "frac_of_nominal_8tbs": build_gbs / roofline.NOMINAL_HBM_GBS,
+        },
+        "build_ms_per_step": build_ms,
+        "phases_ms": ph,
+        "counts": {k: counts[k] for k in ("ks", "kr", "e2")} | {
+            "stencil_entries": int(sum(counts["s_l"].values()))},
+        "clocks": clk,
+        "e2e": e2e,
+        "cpu_baseline": cpu,
+        "parity_vs_reference": parity,
+        "gpu_launches": int(launches),
+        "near_field": nf,
+    }
+    print(json.dumps(line), flush=True)
 
 
 def _numpy_bytes(st) -> int:
@@ -409,13 +452,25 @@ def run_partitioned(args):
     else:
         dist.init_process_group(backend)
     wl = WORKLOADS[args.workload]
-    n_per = wl.n
+    if wl.name == "c5":  # 2^27 + 2^27 per GPU (c5 = 2^30 + 2^30 at 8 GPUs), fixed L = 8
+        n_per = wl.n // 8
+        L = wl.level
+        # generated per shard on the device (torch Philox, seed 1 + rank): a
+        # 2^30 host generation is 24 GB per array
+        g = torch.Generator(device=dev)
+        g.manual_seed(wl.seed + rank)
+        src = torch.rand((n_per, 3), generator=g, device=dev, dtype=torch.float64)
+        recv = torch.rand((n_per, 3), generator=g, device=dev, dtype=torch.float64)
+        q = torch.randn(n_per, generator=g, device=dev, dtype=torch.float64)
+        src_np = q_np = recv_np = None
+    else:
+        n_per = wl.n
+        L = choose_max_level(n_per * ws, 16)
+        src_np, q_np, recv_np = generate(n_per, n_per, wl.dist, wl.seed + rank)
+        src = torch.from_numpy(src_np).to(dev)
+        q = torch.from_numpy(q_np).to(dev)
+        recv = torch.from_numpy(recv_np).to(dev)
     n_glob = n_per * ws
-    L = choose_max_level(n_glob, 16)
-    src_np, q_np, recv_np = generate(n_per, n_per, wl.dist, wl.seed + rank)
-    src = torch.from_numpy(src_np).to(dev)
-    q = torch.from_numpy(q_np).to(dev)
-    recv = torch.from_numpy(recv_np).to(dev)
     comm = D.TorchComm()
     ops = D.DeviceOps()
 
@@ -464,9 +519,9 @@ def run_partitioned(args):
     peak, peak_src = roofline.measured_hbm_gbs(ROOT)
     e2e = None
     if not args.no_e2e:
-        h_src = torch.from_numpy(src_np).pin_memory()
-        h_q = torch.from_numpy(q_np).pin_memory()
-        h_recv = torch.from_numpy(recv_np).pin_memory()
+        h_src = src.cpu().pin_memory()
+        h_q = q.cpu().pin_memory()
+        h_recv = recv.cpu().pin_memory()
         times = []
         d2h = 0
         for _ in range(max(1, args.e2e_steps)):
@@ -532,9 +587,15 @@ def _numpy_bytes_shard(sh) -> int:
 
 def main():
     args = parse()
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.workload is None:
+        args.workload = "c2" if ws == 1 and not args.partitioned else "c5"
     if args.impl == "reference":
         run_reference_arm(args)
-    elif int(os.environ.get("WORLD_SIZE", "1")) > 1:
+    elif ws > 1 or args.partitioned:
+        for k, v in (("MASTER_ADDR", "127.0.0.1"), ("MASTER_PORT", "29531"), ("RANK", "0"),
+                     ("WORLD_SIZE", "1"), ("LOCAL_RANK", "0")):
+            os.environ.setdefault(k, v)
         run_partitioned(args)
     else:
         run_ours(args)

@@ -21,10 +21,15 @@
  * Error codes mirror the reference exception types (errors.py:4-21):
  *   FMMB_ERR_DOMAIN   -> fmmkit.errors.DomainError   (precondition violated)
  *   FMMB_ERR_CAPACITY -> fmmkit.errors.CapacityError (level cap / budget)
- * fmmb_last_error() returns the message of the last failing call on a handle.
+ * fmmb_last_error() returns the message of the calling thread's last failing
+ * call (thread-local text).
  *
- * Threading: a handle may be used from one host thread at a time; calls on
- * different streams with the same handle are allowed (no shared workspace).
+ * Threading: entry points are reentrant, like the reference's nogil kernels
+ * (SURVEY 8(b)).  Each call holds its handle's lock for its duration (the
+ * handle's pinned read-back block, side stream and events are per handle),
+ * so concurrent calls on one handle from several host threads serialise and
+ * each returns exactly what it would return alone; calls on different
+ * streams are allowed (every workspace is per call).
  */
 #ifndef FMMB200_H
 #define FMMB200_H

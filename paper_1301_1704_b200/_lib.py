@@ -144,16 +144,21 @@ def device_of(device=None) -> torch.device:
 
 
 def handle(dev: torch.device) -> int:
+    """The device's library handle (one per device, created once; every C
+    entry point locks it for the duration of the call, so threads may share it)."""
     lib = load()
     idx = dev.index
     h = _handles.get(idx)
     if h is None:
-        out = C.c_void_p()
-        st = lib.fmmb_create(idx, C.byref(out))
-        if st != OK:
-            raise NativeError(f"fmmb_create(device={idx}) failed with status {st}")
-        h = out.value
-        _handles[idx] = h
+        with _lib_lock:
+            h = _handles.get(idx)
+            if h is None:
+                out = C.c_void_p()
+                st = lib.fmmb_create(idx, C.byref(out))
+                if st != OK:
+                    raise NativeError(f"fmmb_create(device={idx}) failed with status {st}")
+                h = out.value
+                _handles[idx] = h
     return h
 
 

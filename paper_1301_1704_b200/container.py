@@ -221,7 +221,9 @@ def read_container(path, device=None) -> tuple:
                 dt = _DTYPES[code]
                 if device is None:
                     arr = np.empty(shape, dtype=dt)
-                    fh.readinto(memoryview(arr.reshape(-1).view(np.uint8)))
+                    got = fh.readinto(memoryview(arr.reshape(-1).view(np.uint8)))
+                    if got != nbytes or arr.nbytes != nbytes:
+                        raise DomainError(f"{path}: truncated structure container")
                     arrays[name] = arr
                 else:
                     arrays[name] = _upload(fh, nbytes, dt, shape, device)
@@ -229,27 +231,39 @@ def read_container(path, device=None) -> tuple:
         return max_level, sections
 
 
-_UP = {}
+_UP_LOCAL = threading.local()
 
 
 def _upload(fh, nbytes: int, dt, shape, device) -> torch.Tensor:
-    """File bytes -> device tensor through two alternating pinned chunks."""
+    """File bytes -> device tensor through two alternating pinned chunks.
+
+    The chunks are per thread and their last-copy events persist across
+    calls: a chunk is refilled only after the copy that last read it is done
+    (whichever array it belonged to), and the call returns after its own
+    copies completed, so no later host write can race an in-flight H2D."""
     out = torch.empty(nbytes, dtype=torch.uint8, device=device)
-    bufs = _UP.setdefault("bufs", [torch.empty(_CHUNK, dtype=torch.uint8, pin_memory=True)
-                                   for _ in range(2)])
-    evs = [None, None]
+    up = _UP_LOCAL.__dict__
+    if "bufs" not in up:
+        up["bufs"] = [torch.empty(_CHUNK, dtype=torch.uint8, pin_memory=True) for _ in range(2)]
+        up["evs"] = [None, None]
+    bufs, evs = up["bufs"], up["evs"]
     at, k = 0, 0
     stream = torch.cuda.current_stream(out.device)
-    while at < nbytes:
-        n = min(_CHUNK, nbytes - at)
-        if evs[k] is not None:
-            evs[k].synchronize()  # the copy that last used this buffer is done
-        got = fh.readinto(memoryview(bufs[k].numpy())[:n])
-        if got != n:
-            raise DomainError("truncated structure container")
-        out[at:at + n].copy_(bufs[k][:n], non_blocking=True)
-        evs[k] = torch.cuda.Event()
-        evs[k].record(stream)
-        at += n
-        k ^= 1
+    try:
+        while at < nbytes:
+            n = min(_CHUNK, nbytes - at)
+            if evs[k] is not None:
+                evs[k].synchronize()  # the copy that last used this buffer is done
+            got = fh.readinto(memoryview(bufs[k].numpy())[:n])
+            if got != n:
+                raise DomainError("truncated structure container")
+            out[at:at + n].copy_(bufs[k][:n], non_blocking=True)
+            evs[k] = torch.cuda.Event()
+            evs[k].record(stream)
+            at += n
+            k ^= 1
+    finally:
+        for e in evs:
+            if e is not None:
+                e.synchronize()
     return out.view(_NP_TORCH[dt]).reshape(shape)

@@ -75,6 +75,7 @@ extern "C" fmmb_status fmmb_classify_boxes(fmmb_handle_t h, const uint64_t* boxe
                                            int64_t n_units_table, int partition_level,
                                            int critical_level, int nodes, int units_per_node,
                                            int node, int8_t* types, void* stream) {
+  FMMB_GUARD(h);
   using namespace fmmb;
   FMMB_ENTER(h);
   if (level < 2) return fmmb_fail(h, FMMB_ERR_DOMAIN, "octree data start at level 2");

@@ -29,15 +29,18 @@
 using namespace fmmb;
 
 // ------------------------------------------------------------------ handle
+// error text of the calling thread's last failed call (thread-local, so a
+// concurrent caller cannot overwrite it between the failure and the read)
+static thread_local std::string t_err;
+
 fmmb_status fmmb_fail(fmmb_handle_t h, fmmb_status st, const char* fmt, ...) {
-  if (h) {
-    char buf[1024];
-    va_list ap;
-    va_start(ap, fmt);
-    vsnprintf(buf, sizeof(buf), fmt, ap);
-    va_end(ap);
-    h->err = buf;
-  }
+  (void)h;
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  t_err = buf;
   return st;
 }
 
@@ -140,12 +143,13 @@ extern "C" fmmb_status fmmb_destroy(fmmb_handle_t h) {
 }
 
 extern "C" const char* fmmb_last_error(fmmb_handle_t h) {
-  return h ? h->err.c_str() : "null handle";
+  return h ? t_err.c_str() : "null handle";
 }
 
 extern "C" int64_t fmmb_last_launch_count(fmmb_handle_t h) { return h ? h->launches : -1; }
 
 extern "C" fmmb_status fmmb_set_sort_path(fmmb_handle_t h, int path) {
+  FMMB_GUARD(h);
   if (!h || path < 0 || path > 3) return FMMB_ERR_ARG;
   h->sort_path = path;
   return FMMB_OK;
@@ -154,6 +158,7 @@ extern "C" fmmb_status fmmb_set_sort_path(fmmb_handle_t h, int path) {
 extern "C" int fmmb_last_sort_path(fmmb_handle_t h) { return h ? h->last_sort_path : -1; }
 
 extern "C" fmmb_status fmmb_set_overlap(fmmb_handle_t h, int on) {
+  FMMB_GUARD(h);
   if (!h) return FMMB_ERR_ARG;
   h->overlap = on != 0;
   return FMMB_OK;
@@ -270,6 +275,18 @@ void launch_hs(const double* src, const double* q, const double* recv, const Buc
 
 // speculative regions apply when the coarse buckets already fit the count path
 inline bool spec_possible(const BucketGeo& g) { return g.shift <= kLcSmallBits; }
+
+// the local pass's LSD fallback sorts (in-bucket key bits, combined index) as
+// one 64-bit composite: every final bucket's key span plus the index bits
+// must fit, else the build takes the Onesweep path (L = 20 with ~2^28
+// points).  Wide coarse buckets are always refined along kRefBits more key
+// bits (k_bkt_plan: one sub-bin per final bucket once the sub-bins span
+// >= 2^kLcSmallBits keys).
+inline bool bucket_fits(const BucketGeo& g) {
+  const int span_bits = g.shift > kLcSmallBits ? std::max(g.shift - kRefBits, kLcSmallBits)
+                                               : g.shift;
+  return span_bits + g.cbits <= 64;
+}
 
 fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int64_t n,
                         const double* recv, int64_t m, int L, const LocalOut& o, bool heads,
@@ -537,7 +554,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
   }
 
   int64_t launches = 0;
-  bool fast = h->sort_path != 2 && tot > 0;
+  bool fast = h->sort_path != 2 && tot > 0 && bucket_fits(bucket_geo(L, n, m, h->num_sms));
   // speculative bucket regions (no histogram pass) unless this shape missed last time
   bool spec = fast && h->sort_path != 3 && spec_possible(bucket_geo(L, n, m, h->num_sms)) &&
               !(h->spec_miss_level == L && h->spec_miss_n == n && h->spec_miss_m == m);
@@ -829,6 +846,7 @@ extern "C" fmmb_status fmmb_build_all(fmmb_handle_t h, const double* src, const 
                                       int64_t n, const double* recv, int64_t m, int level,
                                       fmmb_alloc_fn alloc, void* ctx, fmmb_structures* out,
                                       void** timing, void* stream) {
+  FMMB_GUARD(h);
   fmmb_status st = check_build_args(h, src, n, recv, m, level, alloc, true);
   if (st != FMMB_OK) return st;
   if (!out) return FMMB_ERR_ARG;
@@ -844,6 +862,7 @@ extern "C" fmmb_status fmmb_sort_points(fmmb_handle_t h, const double* points,
                                         const double* charges, int64_t n, int level,
                                         fmmb_alloc_fn alloc, void* ctx, fmmb_point_set* out,
                                         void* stream) {
+  FMMB_GUARD(h);
   fmmb_status st = check_build_args(h, points, n, nullptr, 0, level, alloc, false);
   if (st != FMMB_OK) return st;
   if (!out) return FMMB_ERR_ARG;

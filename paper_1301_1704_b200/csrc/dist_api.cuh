@@ -8,6 +8,7 @@
 extern "C" fmmb_status fmmb_part_histogram(fmmb_handle_t h, const double* src, int64_t n,
                                            const double* recv, int64_t m, int level, int pbits,
                                            uint32_t* hist, void* stream) {
+  FMMB_GUARD(h);
   if (!h || !hist) return FMMB_ERR_ARG;
   if (level < 1 || level > kMaxLevel)
     return fmmb_fail(h, FMMB_ERR_CAPACITY, "max_level %d outside [1, %d]", level, kMaxLevel);
@@ -44,6 +45,7 @@ extern "C" fmmb_status fmmb_part_pack(fmmb_handle_t h, const double* src, const 
                                       int64_t gbase_src, int64_t gbase_recv, double* sxyz,
                                       double* sq, int64_t* sgid, double* rxyz, int64_t* rgid,
                                       int64_t* counts, void* stream) {
+  FMMB_GUARD(h);
   if (!h || !bin_rank || !counts) return FMMB_ERR_ARG;
   if (nranks < 1 || nranks > kPartMaxRanks)
     return fmmb_fail(h, FMMB_ERR_ARG, "nranks %d outside [1, %d]", nranks, kPartMaxRanks);
@@ -148,6 +150,7 @@ extern "C" fmmb_status fmmb_part_counts(fmmb_handle_t h, const double* src, int6
                                         const double* recv, int64_t m, int level, int pbits,
                                         const uint32_t* bin_rank, int nranks, int64_t* counts,
                                         void* stream) {
+  FMMB_GUARD(h);
   if (!counts) return FMMB_ERR_ARG;
   return part_pass(h, src, nullptr, n, recv, m, level, pbits, bin_rank, nranks, 0, 0, nullptr,
                    counts, (cudaStream_t)stream);
@@ -161,6 +164,7 @@ extern "C" fmmb_status fmmb_part_pack_peer(fmmb_handle_t h, const double* src, c
                                            int64_t* const* sgid, double* const* rxyz,
                                            int64_t* const* rgid, const int64_t* soff,
                                            const int64_t* roff, void* stream) {
+  FMMB_GUARD(h);
   using namespace fmmb;
   if (!h || !sxyz || !sgid || !rxyz || !rgid || !soff || !roff) return FMMB_ERR_ARG;
   if (nranks < 1 || nranks > kPartMaxRanks)
@@ -184,6 +188,7 @@ extern "C" fmmb_status fmmb_dist_sort(fmmb_handle_t h, const double* src, const 
                                       int64_t m, const int64_t* gid_recv, int level,
                                       fmmb_alloc_fn alloc, void* ctx, fmmb_point_set* src_out,
                                       fmmb_point_set* recv_out, uint64_t* bmp, void* stream) {
+  FMMB_GUARD(h);
   fmmb_status st = check_build_args(h, src, n, recv, m, level, alloc, true);
   if (st != FMMB_OK) return st;
   if (!src_out || !recv_out || !bmp || level < 1) return FMMB_ERR_ARG;
@@ -217,6 +222,7 @@ struct DistListsHost {  // pinned read-back of the two synchronisation points
 extern "C" fmmb_status fmmb_dist_lists(fmmb_handle_t h, const uint64_t* gbmp, int level,
                                        uint64_t key_lo, uint64_t key_hi, fmmb_alloc_fn alloc,
                                        void* ctx, fmmb_structures* out, void* stream) {
+  FMMB_GUARD(h);
   if (!h || !gbmp || !alloc || !out) return FMMB_ERR_ARG;
   const int L = level;
   if (L < 1 || L > kMaxLevel) return fmmb_fail(h, FMMB_ERR_CAPACITY, "max_level %d", L);

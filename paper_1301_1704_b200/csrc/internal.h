@@ -2,6 +2,7 @@
 #pragma once
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 
 #include "../../include/fmmb200.h"
@@ -24,8 +25,17 @@ struct fmmb_handle_s {
   void* ev_rank = nullptr;       // rank directory done (caller stream)
   void* ev_side = nullptr;       // side stream's work done
   bool overlap = true;           // FMMB_NO_OVERLAP=1 serialises (A/B)
-  std::string err;
+  // every entry point holds this for its whole call: the pinned read-back
+  // block, the side stream and its events are per handle, so concurrent
+  // callers on one device (the reference's kernels are nogil and reentrant,
+  // SURVEY 8(b) "Threading") are serialised instead of racing on them
+  std::recursive_mutex mu;
 };
+
+// null check + the handle's call lock for the rest of the entry point
+#define FMMB_GUARD(h)                 \
+  if (!(h)) return FMMB_ERR_ARG;      \
+  std::lock_guard<std::recursive_mutex> fmmb_guard_((h)->mu)
 
 constexpr size_t kPinnedBytes = 1 << 16;
 

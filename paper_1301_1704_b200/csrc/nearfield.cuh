@@ -178,6 +178,7 @@ extern "C" fmmb_status fmmb_near_field(fmmb_handle_t h, const double* sx, int64_
                                        const double* ry, int64_t rys, const double* rz,
                                        int64_t rzs, int64_t nr, const int64_t* recv_bookmark,
                                        int64_t n_recv_boxes, double* phi, void* stream) {
+  FMMB_GUARD(h);
   using namespace fmmb;
   FMMB_ENTER(h);
   cudaStream_t s = (cudaStream_t)stream;
@@ -218,6 +219,7 @@ extern "C" fmmb_status fmmb_direct_potentials(fmmb_handle_t h, const double* sx,
                                               const double* rx, int64_t rxs, const double* ry,
                                               int64_t rys, const double* rz, int64_t rzs,
                                               int64_t nr, double* phi, void* stream) {
+  FMMB_GUARD(h);
   using namespace fmmb;
   FMMB_ENTER(h);
   cudaStream_t s = (cudaStream_t)stream;

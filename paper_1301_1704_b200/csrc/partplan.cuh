@@ -51,6 +51,7 @@ extern "C" fmmb_status fmmb_partition_level(fmmb_handle_t h, const uint64_t* rec
                                             const int64_t* recv_counts, int64_t n,
                                             int from_level, int level, int64_t total, int units,
                                             int64_t* bounds, int64_t* cum, void* stream) {
+  FMMB_GUARD(h);
   using namespace fmmb;
   FMMB_ENTER(h);
   cudaStream_t s = (cudaStream_t)stream;

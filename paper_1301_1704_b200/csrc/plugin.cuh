@@ -459,6 +459,7 @@ fmmb_status cuda_status(fmmb_handle_t h, const char* what) {
 
 extern "C" fmmb_status fmmb_spread_bits(fmmb_handle_t h, const uint64_t* v, int64_t n,
                                         uint64_t* out, void* stream) {
+  FMMB_GUARD(h);
   FMMB_ENTER(h);
   if (n > 0) {
     k_spread<<<grid_for(n, 256, h->num_sms), 256, 0, (cudaStream_t)stream>>>(v, n, out);
@@ -469,6 +470,7 @@ extern "C" fmmb_status fmmb_spread_bits(fmmb_handle_t h, const uint64_t* v, int6
 
 extern "C" fmmb_status fmmb_compact_bits(fmmb_handle_t h, const uint64_t* v, int64_t n,
                                          uint64_t* out, void* stream) {
+  FMMB_GUARD(h);
   FMMB_ENTER(h);
   if (n > 0) {
     k_compact<<<grid_for(n, 256, h->num_sms), 256, 0, (cudaStream_t)stream>>>(v, n, out);
@@ -480,6 +482,7 @@ extern "C" fmmb_status fmmb_compact_bits(fmmb_handle_t h, const uint64_t* v, int
 extern "C" fmmb_status fmmb_interleave_coords(fmmb_handle_t h, const uint64_t* ix,
                                               const uint64_t* iy, const uint64_t* iz, int64_t n,
                                               uint64_t* out, void* stream) {
+  FMMB_GUARD(h);
   FMMB_ENTER(h);
   if (n > 0) {
     k_interleave<<<grid_for(n, 256, h->num_sms), 256, 0, (cudaStream_t)stream>>>(ix, iy, iz, n,
@@ -492,6 +495,7 @@ extern "C" fmmb_status fmmb_interleave_coords(fmmb_handle_t h, const uint64_t* i
 extern "C" fmmb_status fmmb_deinterleave_indices(fmmb_handle_t h, const uint64_t* idx, int64_t n,
                                                  uint64_t* ix, uint64_t* iy, uint64_t* iz,
                                                  void* stream) {
+  FMMB_GUARD(h);
   FMMB_ENTER(h);
   if (n > 0) {
     k_deinterleave<<<grid_for(n, 256, h->num_sms), 256, 0, (cudaStream_t)stream>>>(idx, n, ix,
@@ -505,6 +509,7 @@ extern "C" fmmb_status fmmb_encode_points(fmmb_handle_t h, const double* x, int6
                                           const double* y, int64_t ys, const double* z,
                                           int64_t zs, int64_t n, int level, uint64_t* out,
                                           void* stream) {
+  FMMB_GUARD(h);
   FMMB_ENTER(h);
   if (level < 0 || level > kMaxLevel)
     return fmmb_fail(h, FMMB_ERR_CAPACITY, "level %d outside [0, %d]", level, kMaxLevel);
@@ -519,6 +524,7 @@ extern "C" fmmb_status fmmb_encode_points(fmmb_handle_t h, const double* x, int6
 extern "C" fmmb_status fmmb_assign_box_ranks(fmmb_handle_t h, const uint64_t* boxes, int64_t n,
                                              int64_t nbins, int64_t* bins, int64_t* ranks,
                                              void* stream) {
+  FMMB_GUARD(h);
   FMMB_ENTER(h);
   cudaStream_t s = (cudaStream_t)stream;
   if (nbins < 1) return fmmb_fail(h, FMMB_ERR_DOMAIN, "nbins must be positive");
@@ -566,6 +572,7 @@ extern "C" fmmb_status fmmb_assign_box_ranks(fmmb_handle_t h, const uint64_t* bo
 
 extern "C" fmmb_status fmmb_exclusive_scan_i64(fmmb_handle_t h, const int64_t* values, int64_t n,
                                                int64_t* out, int64_t* total, void* stream) {
+  FMMB_GUARD(h);
   FMMB_ENTER(h);
   cudaStream_t s = (cudaStream_t)stream;
   Workspace ws(s);
@@ -584,6 +591,7 @@ extern "C" fmmb_status fmmb_exclusive_scan_i64(fmmb_handle_t h, const int64_t* v
 extern "C" fmmb_status fmmb_propagate_to_parents(fmmb_handle_t h, const uint64_t* boxes,
                                                  int64_t n, uint64_t* out, int64_t* count,
                                                  void* stream) {
+  FMMB_GUARD(h);
   FMMB_ENTER(h);
   cudaStream_t s = (cudaStream_t)stream;
   if (n == 0) {
@@ -674,6 +682,7 @@ extern "C" fmmb_status fmmb_adjacent_segments(fmmb_handle_t h, const uint64_t* r
                                               const uint64_t* src, int64_t ns, int level,
                                               int64_t* bookmark, fmmb_alloc_fn alloc, void* ctx,
                                               int64_t** list, int64_t* total, void* stream) {
+  FMMB_GUARD(h);
   FMMB_ENTER(h);
   if (!bookmark || !alloc || !list || !total) return FMMB_ERR_ARG;
   return segments_impl<false>(h, recv, nr, src, ns, level, bookmark, alloc, ctx, list, nullptr,
@@ -685,6 +694,7 @@ extern "C" fmmb_status fmmb_stencil_segments(fmmb_handle_t h, const uint64_t* re
                                              int64_t* bookmark, fmmb_alloc_fn alloc, void* ctx,
                                              int64_t** ranks, int16_t** codes, int64_t* total,
                                              void* stream) {
+  FMMB_GUARD(h);
   FMMB_ENTER(h);
   if (!bookmark || !alloc || !ranks || !codes || !total) return FMMB_ERR_ARG;
   return segments_impl<true>(h, recv, nr, src, ns, level, bookmark, alloc, ctx, ranks, codes,

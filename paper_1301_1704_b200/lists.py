@@ -285,28 +285,31 @@ def _bitmap_path_ok(level: int, n_total: int) -> bool:
 
 def _build_all_sparse(src, q, recv, max_level) -> FmmStructures:
     """Deep levels with few points (occupancy bitmaps would dwarf the data):
-    same outputs from the sorted-search list kernels, level by level."""
-    import time
-
+    same outputs from the sorted-search list kernels, level by level.  Phase
+    times are CUDA-event intervals on the build stream."""
     from .pseudosort import sort_points_device
 
-    t0 = time.perf_counter()
+    dev = src.device
+    stream = torch.cuda.current_stream(dev)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+    ev[0].record(stream)
     ssrc = sort_points_device(src, q, max_level)
-    t1 = time.perf_counter()
+    ev[1].record(stream)
     srecv = sort_points_device(recv, None, max_level)
-    t2 = time.perf_counter()
+    ev[2].record(stream)
     table = build_neighbor_table(ssrc.non_empty_index, srecv.non_empty_index, max_level)
-    t3 = time.perf_counter()
+    ev[3].record(stream)
     directory = build_level_directory(ssrc.non_empty_index, srecv.non_empty_index, max_level)
-    t4 = time.perf_counter()
+    ev[4].record(stream)
     stencils = build_translation_stencils(directory)
-    t5 = time.perf_counter()
+    ev[5].record(stream)
+    ev[5].synchronize()
+    t = [ev[i].elapsed_time(ev[i + 1]) * 1e-3 for i in range(5)]
     return FmmStructures(
         max_level=max_level, sorted_src=ssrc, sorted_recv=srecv, neighbor_table=table,
         directory=directory, stencils=stencils,
-        build_seconds={"sort_sources": t1 - t0, "sort_receivers": t2 - t1,
-                       "neighbor_table": t3 - t2, "level_directory": t4 - t3,
-                       "stencils": t5 - t4},
+        build_seconds={"sort_sources": t[0], "sort_receivers": t[1],
+                       "neighbor_table": t[2], "level_directory": t[3], "stencils": t[4]},
     )
 
 

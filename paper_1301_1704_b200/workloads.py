@@ -60,3 +60,41 @@ WORKLOADS = {
 def perturb(points: np.ndarray, rng: np.random.Generator, scale: float = 1e-3) -> np.ndarray:
     """c4 dynamic-rebuild step: x <- mod(x + N(0, scale), 1.0)."""
     return np.mod(points + rng.normal(scale=scale, size=points.shape), 1.0)
+
+
+# coordinates whose perturbed value np.mod maps to exactly 1.0 (x + noise a
+# tiny negative number): the clamp edge of the encoder (_ckernels.pyx:97-102)
+C4_EDGE_SLOTS = ((5, 0), (77, 1), (4242, 2), (31337, 0), (31337, 1), (31337, 2))
+
+
+def c4_step_inputs(n: int = 2**23, seed: int = 4, steps: int = 1):
+    """Inputs of the c4 golden rebuild step: generate(n, n, uniform, seed),
+    then `steps` perturbations of src and recv drawn from default_rng(123)
+    (src first, then recv, as the trajectory driver), with C4_EDGE_SLOTS set
+    to np.mod(-1e-18, 1.0) == 1.0 on both sets so the clamp edge is always
+    present (a random perturbation reaches it with probability ~1e-9)."""
+    src, q, recv = generate(n, n, "uniform", seed)
+    rng = np.random.default_rng(123)
+    for _ in range(steps):
+        src = perturb(src, rng)
+        recv = perturb(recv, rng)
+    edge = np.mod(np.float64(-1e-18), 1.0)
+    for i, j in C4_EDGE_SLOTS:
+        if i < n:
+            src[i, j] = edge
+            recv[i, j] = edge
+    return src, q, recv
+
+
+def perturb_device(points, gen, scale: float = 1e-3):
+    """c4 rebuild step on the device, in place: x <- remainder(x + N(0, scale), 1.0)
+    (torch's float remainder is fmod plus the sign fix-up, the same
+    operations as np.mod, so a tiny negative sum maps to exactly 1.0 too).
+    `gen` is a CUDA torch.Generator; the trajectory is reproducible from its
+    seed.  Workload driver only (not part of the build path)."""
+    import torch
+
+    noise = torch.randn(points.shape, generator=gen, device=points.device, dtype=points.dtype)
+    points.add_(noise.mul_(scale))
+    torch.remainder(points, 1.0, out=points)
+    return points

@@ -92,3 +92,16 @@ def nearfield() -> dict:
 def nearfield_hashes() -> dict:
     with open(os.path.join(HERE, "nearfield_hashes.json")) as f:
         return json.load(f)
+
+
+def northstar_inputs(name: str):
+    """Inputs of the north-star golden cases (make_golden_northstar.py): the
+    bench's c2 / c3 arrays, and one perturbed c4 rebuild step."""
+    from paper_1301_1704_b200.workloads import WORKLOADS, c4_step_inputs, generate
+
+    wl = WORKLOADS[name]
+    if name == "c4":
+        src, q, recv = c4_step_inputs(wl.n, wl.seed, 1)
+    else:
+        src, q, recv = generate(wl.n, wl.n, wl.dist, wl.seed)
+    return src, q, recv, wl.level

@@ -127,3 +127,50 @@ def test_boundary_coordinates(gpu, ref):
         want = ref.build_all(pts, np.arange(8.0), pts[::-1].copy(), max_level=level)
         got = gpu.build_all(pts, np.arange(8.0), pts[::-1].copy(), max_level=level)
         assert not compare_structures(got, want), level
+
+
+def _reference_sparse(ref, src, q, recv, level):
+    """The reference's build_all at levels whose dense 8^L histogram cannot be
+    allocated (L >= 12): the same steps with the histogram rank replaced by
+    the stable argsort it equals (the reference's own oracle,
+    tests/test_pseudosort.py:94-104); encode, the level directory, E2 and E4
+    are the reference's own functions (lists.py:69-130, compiled kernels)."""
+    from types import SimpleNamespace
+
+    k = ref.backend.kernels
+
+    def sort(pts, charges):
+        boxes = k.encode_points(pts[:, 0], pts[:, 1], pts[:, 2], level)
+        perm = np.argsort(boxes, kind="stable").astype(np.int64)
+        sb = boxes[perm]
+        head = np.ones(sb.shape[0], dtype=bool)
+        head[1:] = sb[1:] != sb[:-1]
+        starts = np.flatnonzero(head).astype(np.int64)
+        bm = np.append(starts, np.int64(sb.shape[0]))
+        return SimpleNamespace(level=level, points=pts[perm],
+                               charges=None if charges is None else charges[perm],
+                               permutation=perm, bookmarks=bm, non_empty_index=sb[starts],
+                               boxes=sb)
+
+    ss, sr = sort(src, q), sort(recv, None)
+    table = ref.lists.build_neighbor_table(ss.non_empty_index, sr.non_empty_index, level)
+    directory = ref.lists.build_level_directory(ss.non_empty_index, sr.non_empty_index, level)
+    stencils = ref.lists.build_translation_stencils(directory)
+    return SimpleNamespace(max_level=level, sorted_src=ss, sorted_recv=sr, neighbor_table=table,
+                           directory=directory, stencils=stencils)
+
+
+@pytest.mark.parametrize("n,m,level,seed", [(3000, 2500, 13, 5), (2000, 1800, 20, 6),
+                                            (40000, 30000, 13, 7)])
+def test_build_all_deep_levels(gpu, ref, n, m, level, seed):
+    """The sparse build (levels above the occupancy-bitmap limit,
+    lists._build_all_sparse) against the reference's own steps."""
+    src, q, _ = generate(n, 1, "sphere", seed)
+    _, _, recv = generate(1, m, "sphere", seed + 1000)
+    want = _reference_sparse(ref, src, q, recv, level)
+    got = gpu.build_all(src, q, recv, max_level=level, histogram_budget_bytes=8 ** level * 8)
+    errors = compare_structures(got, want)
+    assert not errors, "\n".join(errors)
+    bs = got.build_seconds
+    assert set(bs) >= {"sort_sources", "sort_receivers", "neighbor_table", "level_directory",
+                       "stencils"} and all(v >= 0 for v in bs.values())
