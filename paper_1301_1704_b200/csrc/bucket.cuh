@@ -94,11 +94,15 @@ __device__ __forceinline__ uint32_t bucket_of(uint64_t key, int is_recv, const B
 }
 
 // ---------------------------------------------------------------- H pass --
+// With `fine` non-null (wide geometries, where every non-empty coarse bucket
+// is refined) the same read also counts every point's refinement sub-bin
+// (global atomics into fine[bucket][sub]), so k_bkt_fine's second read of the
+// inputs is skipped.
 template <bool NARROW>
 __global__ void __launch_bounds__(kHThreads)
     k_bkt_hist(const double* __restrict__ src, const double* __restrict__ recv,
                const BucketGeo g, int level, uint32_t* __restrict__ mat,
-               uint32_t* __restrict__ err) {
+               uint32_t* __restrict__ err, uint32_t* __restrict__ fine) {
   extern __shared__ uint32_t s_hist[];  // [nb]
   const int lane = threadIdx.x & 31;
   for (int b = threadIdx.x; b < g.nb; b += kHThreads) s_hist[b] = 0;
@@ -128,7 +132,13 @@ __global__ void __launch_bounds__(kHThreads)
       if (i < tot) {
         const uint64_t key = encode_any<NARROW>(x[k], y[k], z[k], level, grid);
         bad |= key >= lim;
-        atomicAdd(&s_hist[bucket_of(key & (lim - 1), i >= g.n, g)], 1u);
+        const uint32_t b = bucket_of(key & (lim - 1), i >= g.n, g);
+        atomicAdd(&s_hist[b], 1u);
+        if (fine) {
+          const int R = g.shift < 8 ? g.shift : 8;  // = ref_bits(g)
+          const uint32_t sub = (uint32_t)(((key & (lim - 1)) >> (g.shift - R)) & ((1u << R) - 1u));
+          atomicAdd(fine + (size_t)b * 256 + sub, 1u);  // 256 = kRefBins
+        }
       }
     }
   }
@@ -245,7 +255,8 @@ __global__ void __launch_bounds__(256)
     k_bkt_fine(const double* __restrict__ src, const double* __restrict__ recv,
                const BucketGeo g, int level, const uint32_t* __restrict__ bstart,
                const uint32_t* __restrict__ maxb, uint32_t cap, uint32_t* __restrict__ fine) {
-  if (__ldg(maxb) <= cap && !wide_buckets(g)) return;
+  // nothing to refine, or wide geometry (the H pass already counted the sub-bins)
+  if ((__ldg(maxb) <= cap && !wide_buckets(g)) || wide_buckets(g)) return;
   const int64_t tot = g.n + g.m;
   const uint64_t kmask = (1ull << g.sbits) - 1ull;
   const double grid = (double)(1ll << level);
@@ -532,7 +543,6 @@ __global__ void __launch_bounds__(kSThreads, 1)
     if (is_src && base + rows > n) return false;  // straddles src | recv
     const double* rp = row_ptr(src, recv, n, base);
     if (((uintptr_t)rp & 15) || ((rows * 24) & 15)) return false;
-    if (is_src && q && (((uintptr_t)(q + base) & 15) || ((rows * 8) & 15))) return false;
     return true;
   };
   auto produce = [&](int k) {  // thread 0 only
@@ -542,11 +552,9 @@ __global__ void __launch_bounds__(kSThreads, 1)
       const int64_t base = lo + (int64_t)k * kSRows;
       const int rows = stage_rows(k);
       double* xyz = stage_xyz(k);
-      const bool with_q = base < n && q;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(full + st, rows * 24 + (with_q ? rows * 8 : 0));
+      mbar_expect_tx(full + st, rows * 24);
       bulk_g2s(xyz, row_ptr(src, recv, n, base), rows * 24, full + st);
-      if (with_q) bulk_g2s(xyz + 3 * kSRows, q + base, rows * 8, full + st);
     } else {
       mbar_arrive(full + st);  // consumers fill this stage themselves
     }
@@ -563,7 +571,6 @@ __global__ void __launch_bounds__(kSThreads, 1)
       xyz[3 * tid] = __ldg(p);
       xyz[3 * tid + 1] = __ldg(p + 1);
       xyz[3 * tid + 2] = __ldg(p + 2);
-      if (i < n) xyz[3 * kSRows + tid] = q ? __ldg(q + i) : 0.0;
     }
     const uint64_t raw =
         encode_any<NARROW>(xyz[3 * tid], xyz[3 * tid + 1], xyz[3 * tid + 2], level, grid);
@@ -588,9 +595,10 @@ __global__ void __launch_bounds__(kSThreads, 1)
     const double* xyz = stage_xyz(k);
     const int64_t i = lo + (int64_t)k * kSRows + tid;
     if (tid < stage_rows(k) && dst != 0xFFFFFFFFu) {
-      const double w = i < n ? (q ? xyz[3 * kSRows + tid] : 0.0) : __longlong_as_double(i - n);
+      // record = {x, y, z, index within its set}: one 32-B store, no side
+      // array (charges follow the permutation in k_gather_q)
+      const double w = __longlong_as_double(i < n ? i : i - n);
       st_v4f64(rec + 4 * (size_t)dst, xyz[3 * tid], xyz[3 * tid + 1], xyz[3 * tid + 2], w);
-      if (i < n) idx[dst] = (uint32_t)i;
     }
     mbar_arrive(empty + k % kSStages);
   };
@@ -805,8 +813,6 @@ __global__ void __launch_bounds__(kLcThreads)
     mbar_expect_tx(bar, bytes);
     bulk_g2s(s_rec, rec + 4 * (size_t)rb, bytes, bar);
   }
-  if (set == 0)
-    for (int j = tid; j < B; j += kLcThreads) s_idx[j] = __ldg(idx + rb + j);
   mbar_wait(bar, bar_phase);
   bar_phase ^= 1u;
   __syncthreads();
@@ -821,7 +827,8 @@ __global__ void __launch_bounds__(kLcThreads)
   for (int j = tid; j < B; j += kLcThreads) {
     const double* r = s_rec + 4 * j;
     const uint64_t key = encode_any<NARROW>(r[0], r[1], r[2], level, grid);
-    const uint32_t ci = set == 0 ? s_idx[j] : (uint32_t)(n + __double_as_longlong(r[3]));
+    const int64_t li = __double_as_longlong(r[3]);  // index within the set
+    const uint32_t ci = (uint32_t)(set ? n + li : li);  // combined input index
     // < span for every valid point; out-of-grid inputs (reported as a DomainError
     // after the build) are clamped so they cannot index outside the bucket
     uint64_t lk = (key & ((1ull << g.sbits) - 1ull)) - prefix;
@@ -865,7 +872,13 @@ __global__ void __launch_bounds__(kLcThreads)
       x += i < warp ? s_red[i] : 0u;
       mx = s_red[kLcWarps + i] > mx ? s_red[kLcWarps + i] : mx;
     }
-    ranked = mx <= 64;
+    // every point is ranked inside its box by counting the smaller combined
+    // indices of the box (O(box size) per point; a box of the whole bucket
+    // costs kLcCap^2 / kLcThreads compares per thread, ~10 us): the LSD
+    // fallback is never needed here, so CK only has to hold the composite
+    // keys of the wide-bucket path (host: ck32)
+    ranked = true;
+    (void)mx;
     uint32_t start = x & 0xFFFFu, hidx = x >> 16;
     unsigned long long* bm = set ? o.bmp[1] : o.bmp[0];
     uint32_t* hp = idx + rb;
@@ -918,12 +931,7 @@ __global__ void __launch_bounds__(kLcThreads)
       const int j = p0[pos];
       const double* r = s_rec + 4 * j;
       store_row(o.pts, p, r[0], r[1], r[2]);
-      if (set == 0) {
-        if (o.q) o.q[p] = r[3];
-        o.perm[p] = perm_of(o, 0, (int64_t)s_idx[j]);
-      } else {
-        o.perm[p] = perm_of(o, 1, __double_as_longlong(r[3]));
-      }
+      o.perm[p] = perm_of(o, set, __double_as_longlong(r[3]));
       o.boxes[p] = prefix + (uint64_t)k0[j];
     }
     __syncthreads();  // smem reused by the next bucket
@@ -999,12 +1007,7 @@ __global__ void __launch_bounds__(kLcThreads)
       const double* r = s_rec + 4 * pl;
       const uint64_t mk = prefix + lk;
       store_row(o.pts, p, r[0], r[1], r[2]);
-      if (set == 0) {
-        if (o.q) o.q[p] = r[3];
-        o.perm[p] = perm_of(o, 0, (int64_t)s_idx[pl]);
-      } else {
-        o.perm[p] = perm_of(o, 1, __double_as_longlong(r[3]));
-      }
+      o.perm[p] = perm_of(o, set, __double_as_longlong(r[3]));
       o.boxes[p] = mk;
       const int64_t incl = hbase + woff + __popc(hb & (lt | (1u << lane)));
       if (head) {
@@ -1037,6 +1040,36 @@ __global__ void __launch_bounds__(kLcThreads)
     __syncthreads();  // s_red[8..] reused by the next chunk
   }
   }  // final buckets
+}
+
+// sorted charges: q_out[p] = q[perm[p]] for the n source positions (the
+// bucket records carry the index, not the charge); four independent
+// gathers in flight per thread.  Runs before k_gid_map (perm is still the
+// local index then).
+__global__ void __launch_bounds__(256)
+    k_gather_q(const int64_t* __restrict__ perm, const double* __restrict__ q, int64_t n,
+               double* __restrict__ q_out, const uint32_t* __restrict__ fail) {
+  if (__ldg(fail)) return;  // the sort reruns on the general path
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x * 4;
+  for (int64_t b = (int64_t)blockIdx.x * blockDim.x * 4 + threadIdx.x; b < n; b += stride) {
+    int64_t v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t p = b + (int64_t)k * blockDim.x;
+      v[k] = p < n ? __ldcs(perm + p) : 0;
+    }
+    double w[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t p = b + (int64_t)k * blockDim.x;
+      w[k] = p < n ? __ldg(q + v[k]) : 0.0;
+    }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int64_t p = b + (int64_t)k * blockDim.x;
+      if (p < n) __stcs(q_out + p, w[k]);
+    }
+  }
 }
 
 // perm[p] = gid[perm[p]] of its set (multi-GPU: local -> global input index);

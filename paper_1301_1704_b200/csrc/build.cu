@@ -16,6 +16,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <functional>
 #include <vector>
 
 #include "internal.h"
@@ -80,6 +81,11 @@ extern "C" fmmb_status fmmb_create(int device, fmmb_handle_t* out) {
     h->ev_rank = e[1];
     h->ev_side = e[2];
     h->overlap = getenv("FMMB_NO_OVERLAP") == nullptr;
+    const char* lw = getenv("FMMB_LW");
+    h->list_writer = lw ? atoi(lw) : 1;
+    h->local_after_count = getenv("FMMB_LOCAL_AFTER") != nullptr;
+    const char* lc = getenv("FMMB_LC_PER_SM");
+    h->lc_per_sm = lc ? atoi(lc) : 0;
   }
   // stream-ordered pool: keep freed workspace for reuse across calls
   cudaMemPool_t pool;
@@ -104,6 +110,8 @@ extern "C" fmmb_status fmmb_create(int device, fmmb_handle_t* out) {
                        (int)scatter_smem_bytes());
   cudaFuncSetAttribute(k_bkt_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)scatter_smem_bytes());
+  cudaFuncSetAttribute(k_lists_write_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)sw_smem_bytes());
   cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(sizeof(uint32_t) << kPartMaxBits));
 #define FMMB_LCATTR(CK, NW, HD)                                                        \
@@ -212,6 +220,7 @@ struct BuildPlanHost {  // mirrored in the pinned readback block
 
 // ---- sort phase, fast path: payload-carrying bucket sort (bucket.cuh)
 struct BucketRun {  // scratch that outlives the sort phase (heads pass)
+  std::function<void(cudaStream_t)> local;  // the local pass (+ gid map), launched by the caller
   char* scratch = nullptr;
   BucketGeo g{};
   const uint32_t* bstart_f = nullptr;
@@ -229,6 +238,7 @@ void launch_local(fmmb_handle_t h, const double* rec, uint32_t* idx, const uint3
   auto kern = k_bkt_local<CK, NARROW, HEADS>;
   int per_sm = 1;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLcThreads, lc_smem_bytes<CK>());
+  if (h->lc_per_sm > 0) per_sm = std::min(per_sm, h->lc_per_sm);
   const int grid = std::max(1, per_sm) * h->num_sms;  // persistent: all CTAs resident
   kern<<<grid, kLcThreads, lc_smem_bytes<CK>(), s>>>(rec, idx, bstart_f, rbase, desc, nfinal, g,
                                                      L, o, lst, fail);
@@ -261,11 +271,14 @@ void launch_hs(const double* src, const double* q, const double* recv, const Buc
                int num_sms, int L, uint32_t* mat, uint32_t* bstart, uint64_t* sst, uint32_t* ctl,
                uint32_t* fine, const PlanOut& po, double* rec, uint32_t* idx, uint32_t* err,
                cudaStream_t s, unsigned long long* const* sbmp) {
-  k_bkt_hist<NARROW><<<(unsigned)g.hgrid, kHThreads, (size_t)g.nb * 4, s>>>(src, recv, g, L,
-                                                                             mat, err);
+  const bool wide = g.shift > kLcSmallBits;  // every non-empty bucket is refined
+  k_bkt_hist<NARROW><<<(unsigned)g.hgrid, kHThreads, (size_t)g.nb * 4, s>>>(
+      src, recv, g, L, mat, err, wide ? fine : nullptr);
   k_bkt_scan<<<(unsigned)ceil_div(g.nb, kScanBuckets), 256, 0, s>>>(mat, g, bstart, sst,
                                                                     ctl + 0, ctl + 2);
-  k_bkt_fine<NARROW><<<num_sms * 8, 256, 0, s>>>(src, recv, g, L, bstart, ctl + 2, kLcCap, fine);
+  if (!wide)
+    k_bkt_fine<NARROW><<<num_sms * 8, 256, 0, s>>>(src, recv, g, L, bstart, ctl + 2, kLcCap,
+                                                   fine);
   k_bkt_plan<<<(unsigned)ceil_div(g.nb, 256), 256, 0, s>>>(g, bstart, ctl + 2, kLcCap, fine, po);
   const int sgrid = (int)std::min<int64_t>(num_sms, ceil_div(g.n + g.m, kSRows));
   const FinalMap fm{po.fbase, po.gtab, ctl + 2, kLcCap, 0u, nullptr, nullptr, {sbmp[0], sbmp[1]}};
@@ -282,11 +295,10 @@ inline bool spec_possible(const BucketGeo& g) { return g.shift <= kLcSmallBits; 
 // points).  Wide coarse buckets are always refined along kRefBits more key
 // bits (k_bkt_plan: one sub-bin per final bucket once the sub-bins span
 // >= 2^kLcSmallBits keys).
-inline bool bucket_fits(const BucketGeo& g) {
-  const int span_bits = g.shift > kLcSmallBits ? std::max(g.shift - kRefBits, kLcSmallBits)
-                                               : g.shift;
-  return span_bits + g.cbits <= 64;
+inline int final_span_bits(const BucketGeo& g) {
+  return g.shift > kLcSmallBits ? std::max(g.shift - kRefBits, kLcSmallBits) : g.shift;
 }
+inline bool bucket_fits(const BucketGeo& g) { return final_span_bits(g) + g.cbits <= 64; }
 
 fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int64_t n,
                         const double* recv, int64_t m, int L, const LocalOut& o, bool heads,
@@ -355,7 +367,13 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
   // the scatter set the occupancy bits: from here the local pass (on `ls`)
   // and the caller's stream (directory, lists) proceed independently
   const uint32_t* lfail = spec ? &dplan->spec_fail : po.fail;
-  const bool ck32 = g.shift + g.cbits <= 32;
+  // CK holds the LSD composite (in-bucket key bits, combined index) of final
+  // buckets wider than the box-count path; with HEADS every final bucket
+  // spans <= 2^kLcSmallBits keys unless the refined sub-bins are wider, and
+  // the box-count path ranks without composites, so 32-bit CK (less shared
+  // memory: 3 resident CTAs per SM instead of 2) is enough
+  const bool lsd_possible = !heads || final_span_bits(g) > kLcSmallBits;
+  const bool ck32 = !lsd_possible || g.shift + g.cbits <= 32;
   // multi-GPU: the local pass writes local input indices; their global
   // indices follow in one high-occupancy gather (k_gid_map) instead of
   // latency-exposed lookups inside the local pass
@@ -375,16 +393,16 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
       else { if (ck32) FMMB_LOCAL(uint32_t, false, false); else FMMB_LOCAL(uint64_t, false, false); }
     }
 #undef FMMB_LOCAL
+    if (q && n > 0 && o.q)
+      k_gather_q<<<(unsigned)h->num_sms * 16, 256, 0, st>>>(o.perm, q, n, o.q, lfail);
     if (o.gid[0] || o.gid[1])
       k_gid_map<<<(unsigned)h->num_sms * 16, 256, 0, st>>>(o.perm, n, m, o.gid[0], o.gid[1],
                                                             lfail);
   };
-  launches += 6 + ((o.gid[0] || o.gid[1]) ? 1 : 0);
-  if (ls != s) {  // right after the scatter: overlaps the directory, the count and the write
-    cudaEventRecord((cudaEvent_t)h->ev_split, s);
-    cudaStreamWaitEvent(ls, (cudaEvent_t)h->ev_split, 0);
-  }
-  local(ls);
+  // spec: init, scatter, counts, scan; hist: hist, scan, [fine], plan, scatter; + local
+  const int sort_kernels = spec ? 4 : (g.shift > kLcSmallBits ? 4 : 5);
+  launches += sort_kernels + 1 + ((o.gid[0] || o.gid[1]) ? 1 : 0) + ((q && n > 0 && o.q) ? 1 : 0);
+  run.local = local;
   run.scratch = w;
   run.g = g;
   run.bstart_f = po.bstart_f;
@@ -446,6 +464,24 @@ fmmb_status sort_onesweep(fmmb_handle_t h, const double* src, const double* q, i
   ++launches;
   cudaFreeAsync(w, s);
   return FMMB_OK;
+}
+
+// E2/E4 write pass: the staged writer (per-parent shared-memory compaction,
+// 32-B vector stores) unless FMMB_LW=0 selects the per-lane-store writer
+inline void launch_lists_write(fmmb_handle_t h, const ListsParams& lp, const ListsLayout* lay,
+                               int64_t nwork_cap, cudaStream_t s) {
+  if (h->list_writer == 0) {
+    const int lgrid = (int)std::max<int64_t>(
+        1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * 16));
+    k_lists_write<<<lgrid, kLThreads, 0, s>>>(lp, lay);
+    return;
+  }
+  int per_sm = 1;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lists_write_staged, kSwThreads,
+                                                sw_smem_bytes());
+  const int lgrid = (int)std::max<int64_t>(
+      1, std::min<int64_t>(ceil_div(nwork_cap, kSwWarps), (int64_t)h->num_sms * std::max(per_sm, 1)));
+  k_lists_write_staged<<<lgrid, kSwThreads, sw_smem_bytes(), s>>>(lp, lay);
 }
 
 // Multi-GPU sort phase extras: global indices of the local points and the
@@ -586,6 +622,19 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
         return st;
       }
     }
+    // the local pass on the side stream: right after the scatter (it then
+    // overlaps the directory, the count and the write), or after the count
+    // when h->local_after_count (A/B knob FMMB_LOCAL_AFTER=1)
+    auto start_local = [&]() {
+      if (!brun.local) return;
+      if (ls != s) {
+        cudaEventRecord((cudaEvent_t)h->ev_split, s);
+        cudaStreamWaitEvent(ls, (cudaEvent_t)h->ev_split, 0);
+      }
+      brun.local(ls);
+      brun.local = nullptr;
+    };
+    if (!h->local_after_count || !lists) start_local();
     if (ev) cudaEventRecord(ev[1], s);
 
     // ---- K5: bitmap pyramid (big levels one launch each, the rest in one CTA)
@@ -661,6 +710,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
           lp, glay, (uint64_t*)W(o_st4), (uint64_t*)W(o_st2), tc + 10, dplan->seg_totals);
       launches += 2;
     }
+    start_local();
     if (brun.scratch) {  // bucket path: bookmarks / non-empty keys at global box ranks
       if (ls != s) {  // heads on the side stream: after the local pass and the rank directory
         cudaEventRecord((cudaEvent_t)h->ev_rank, s);
@@ -779,10 +829,8 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
       lp.ranks_out[k] = (int64_t*)(arena_b + b_r[k]);
       lp.codes_out[k] = (int16_t*)(arena_b + b_c[k]);
     }
-    const int lgrid = (int)std::max<int64_t>(
-        1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * 16));
     if (ev) cudaEventRecord(ev[4], s);
-    k_lists_write<<<lgrid, kLThreads, 0, s>>>(lp, (const ListsLayout*)W(o_lay));
+    launch_lists_write(h, lp, (const ListsLayout*)W(o_lay), nwork_cap, s);
     ++launches;
     if (ev) cudaEventRecord(ev[5], s);  // the write kernel alone (before the side join)
 

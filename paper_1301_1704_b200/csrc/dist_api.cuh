@@ -377,10 +377,7 @@ extern "C" fmmb_status fmmb_dist_lists(fmmb_handle_t h, const uint64_t* gbmp, in
     lp.ranks_out[k] = (int64_t*)(arena_b + b_r[k]);
     lp.codes_out[k] = (int16_t*)(arena_b + b_c[k]);
   }
-  const int64_t nwork = h1.lay.work_off[L + 1];
-  const int lgrid = (int)std::max<int64_t>(
-      1, std::min<int64_t>(ceil_div(nwork, kLWarps), (int64_t)h->num_sms * 16));
-  k_lists_write<<<lgrid, kLThreads, 0, s>>>(lp, glay);
+  launch_lists_write(h, lp, glay, h1.lay.work_off[L + 1], s);
   ++h->launches;
 
   memset(out, 0, sizeof(*out));

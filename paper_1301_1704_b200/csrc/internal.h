@@ -25,6 +25,9 @@ struct fmmb_handle_s {
   void* ev_rank = nullptr;       // rank directory done (caller stream)
   void* ev_side = nullptr;       // side stream's work done
   bool overlap = true;           // FMMB_NO_OVERLAP=1 serialises (A/B)
+  bool local_after_count = false;  // FMMB_LOCAL_AFTER=1: local pass after the list count (A/B)
+  int lc_per_sm = 0;             // FMMB_LC_PER_SM: cap on resident local-pass CTAs per SM (A/B)
+  int list_writer = 1;           // 1 staged (default), 0 per-lane stores (FMMB_LW=0, A/B)
   // every entry point holds this for its whole call: the pinned read-back
   // block, the side stream and its events are per handle, so concurrent
   // callers on one device (the reference's kernels are nogil and reentrant,

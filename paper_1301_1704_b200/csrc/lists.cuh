@@ -377,6 +377,228 @@ __global__ void __launch_bounds__(kLThreads)
   }
 }
 
+// ------------------------------------------------------ staged write ----
+// Write pass, staged: a warp compacts ALL rows of its receiver parent P (the
+// owned child rows are consecutive in every CSR, so P's E4 entries, codes
+// and E2 entries are three contiguous output ranges) into its shared-memory
+// slice -- u32 ranks (box ranks < 2^31), i16 codes -- and then streams each
+// range out as 32-byte aligned vector stores (lane = one 32-B unit, a warp
+// store = 1 KB of full L2 lines); only the unaligned first / last unit of a
+// range is stored element-wise.  Same enumeration and ballot compaction as
+// write_rows, but the compaction targets shared memory, so HBM sees full-line
+// writes instead of per-lane 8-B / 2-B stores at arbitrary alignment.
+#ifndef FMMB_SWWARPS
+#define FMMB_SWWARPS 8
+#endif
+constexpr int kSwWarps = FMMB_SWWARPS;
+constexpr int kSwThreads = kSwWarps * 32;
+constexpr int kSwE4 = 8 * 189;  // an E4 row holds <= 216 - 27 entries
+constexpr int kSwE2 = 8 * 27;
+struct __align__(32) SwBuf {
+  uint32_t r4[kSwE4 + 8];
+  uint32_t r2[kSwE2 + 8];
+  int16_t c4[kSwE4 + 32];
+  uint32_t slot_word[32];  // occupied window slots, compacted in key order
+  uint32_t slot_first[32];
+};
+__host__ __device__ constexpr size_t sw_smem_bytes() { return sizeof(SwBuf) * kSwWarps; }
+
+__device__ __forceinline__ void st_v4_b64(void* p, uint64_t a, uint64_t b, uint64_t c,
+                                          uint64_t d) {
+#ifdef FMMB_LW_CS
+  asm volatile("st.global.cs.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c),
+               "l"(d)
+               : "memory");
+#else
+  asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c),
+               "l"(d)
+               : "memory");
+#endif
+}
+
+template <bool E4, bool E2>
+__device__ __forceinline__ void stage_rows(uint32_t rm, const uint32_t (&meta)[7],
+                                           const uint32_t (&rank)[7], int nch, SwBuf& b,
+                                           int& k4, int& k2, int o4, int o4c, int o2) {
+  const unsigned lt = lanemask_lt();
+  uint32_t rbits = rm;
+  while (rbits) {
+    const int cr = __ffs(rbits) - 1;
+    rbits &= rbits - 1;
+    const int crw = (cr & 1) + 7 * ((cr >> 1) & 1) + 49 * ((cr >> 2) & 1);
+    const int sh = 1 + cr;
+#pragma unroll
+    for (int ch = 0; ch < 7; ++ch) {
+      if (ch >= nch) break;  // warp-uniform: only chunks holding occupied slots
+      const uint32_t m = meta[ch];
+      const uint32_t nb = m >> sh;
+      if (E4) {
+        const unsigned v = m & ~nb & 1u;
+        const unsigned bl = ballot_full(v);
+        if (v) {
+          const int at = k4 + __popc(bl & lt);
+          b.r4[o4 + at] = rank[ch];
+          b.c4[o4c + at] = (int16_t)((int)(m >> 9) - crw);
+        }
+        k4 += __popc(bl);
+      }
+      if (E2) {
+        const unsigned v = m & nb & 1u;
+        const unsigned bl = ballot_full(v);
+        if (v) b.r2[o2 + k2 + __popc(bl & lt)] = rank[ch];
+        k2 += __popc(bl);
+      }
+    }
+  }
+}
+
+// s[o + k] -> g[w + k] for k < T (u32 -> i64); g + (w - o) is 32-B aligned
+__device__ __forceinline__ void flush_ranks(int64_t* __restrict__ g, int64_t w,
+                                            const uint32_t* s, int o, int T, int lane) {
+  int64_t* g0 = g + (w - o);
+  const int end = o + T;
+  for (int i0 = 4 * lane; i0 < end; i0 += 128) {
+    if (i0 >= o && i0 + 4 <= end) {
+      const uint4 v = *reinterpret_cast<const uint4*>(s + i0);
+      st_v4_b64(g0 + i0, v.x, v.y, v.z, v.w);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (i0 + j >= o && i0 + j < end) g0[i0 + j] = (int64_t)s[i0 + j];
+    }
+  }
+}
+
+// codes: 16 per 32-B unit
+__device__ __forceinline__ void flush_codes(int16_t* __restrict__ g, int64_t w, const int16_t* s,
+                                            int o, int T, int lane) {
+  int16_t* g0 = g + (w - o);
+  const int end = o + T;
+  for (int i0 = 16 * lane; i0 < end; i0 += 512) {
+    if (i0 >= o && i0 + 16 <= end) {
+      const ulonglong4 v = *reinterpret_cast<const ulonglong4*>(s + i0);
+      st_v4_b64(g0 + i0, v.x, v.y, v.z, v.w);
+    } else {
+      for (int j = 0; j < 16; ++j)
+        if (i0 + j >= o && i0 + j < end) g0[i0 + j] = s[i0 + j];
+    }
+  }
+}
+
+__device__ __forceinline__ void write_parent_staged(const ListsParams& p, const ListsLayout& lay,
+                                                    int L, int l, int64_t j, int lane, SwBuf& b) {
+  const unsigned FULL = 0xffffffffu;
+  const int c = lane & 7;
+  const int cc = (c & 1) + 7 * ((c >> 1) & 1) + 49 * ((c >> 2) & 1) + 171;
+  const uint64_t P = __ldg(p.rkeys[l - 1] + lay.p_lo[l] + j);
+  uint64_t qk = window_key(P, l, lane);
+  int o = lane;
+#pragma unroll
+  for (int k = 2; k <= 32; k <<= 1) {
+#pragma unroll
+    for (int d = k >> 1; d > 0; d >>= 1) {
+      const uint64_t ok = __shfl_xor_sync(FULL, qk, d);
+      const int oo = __shfl_xor_sync(FULL, o, d);
+      const bool want_min = ((lane & d) == 0) == ((lane & k) == 0);
+      if (want_min ? (ok < qk) : (ok > qk)) {
+        qk = ok;
+        o = oo;
+      }
+    }
+  }
+  uint32_t sm = 0, sfirst = 0;
+  if (qk != ~0ull)
+    children_of(p.bmp + p.bmp_off[0][l], p.dir + p.bmp_off[0][l], qk, sm, sfirst);
+  uint32_t rm, rfirst;
+  children_of(p.bmp + p.bmp_off[1][l], p.dir + p.bmp_off[1][l], P, rm, rfirst);
+  uint32_t own = 0;
+  int64_t r0 = -1;
+  {
+    int64_t r = rfirst;
+#pragma unroll
+    for (int cb = 0; cb < 8; ++cb)
+      if ((rm >> cb) & 1u) {
+        if (r >= lay.r_lo[l] && r < lay.r_hi[l]) {
+          own |= 1u << cb;
+          if (r0 < 0) r0 = r - lay.r_lo[l];
+        }
+        ++r;
+      }
+  }
+  if (!own) return;
+  // occupied window slots (source children present), compacted in key order:
+  // candidate chunk ch covers compacted slots 4ch..4ch+3, so sparse windows
+  // (surfaces, deep levels) visit ceil(slots / 4) chunks instead of 7
+  const unsigned occ_slots = __ballot_sync(FULL, sm != 0u);
+  const int nslot = __popc(occ_slots);
+  if (sm) {
+    const int at = __popc(occ_slots & lanemask_lt());
+    b.slot_word[at] = sm | ((uint32_t)o << 8);
+    b.slot_first[at] = sfirst;
+  }
+  __syncwarp();
+  const int nch = (nslot + 3) >> 2;
+  uint32_t meta[7], rank[7];
+#pragma unroll
+  for (int ch = 0; ch < 7; ++ch) {
+    const int slot = 4 * ch + (lane >> 3);
+    const uint32_t v = slot < nslot ? b.slot_word[slot] : (13u << 8);
+    const uint32_t f = slot < nslot ? b.slot_first[slot] : 0u;
+    const uint32_t smk = v & 0xFFu;
+    const int so = (int)(v >> 8);
+    const uint64_t nw = kNear.w[so];
+    uint32_t nearcr = 0;
+#pragma unroll
+    for (int cr = 0; cr < 8; ++cr) nearcr |= ((uint32_t)(nw >> (8 * cr + c)) & 1u) << cr;
+    const int sx = so % 3 - 1, sy = (so / 3) % 3 - 1, sz = so / 9 - 1;
+    const uint32_t code0 = (uint32_t)(2 * sx + 7 * 2 * sy + 49 * 2 * sz + cc);
+    const bool occ = slot < nslot && ((smk >> c) & 1u);
+    meta[ch] = (occ ? 1u : 0u) | (nearcr << 1) | (code0 << 9);
+    rank[ch] = f + __popc(smk & ((1u << c) - 1u));
+  }
+  const int64_t w4 = l >= 2 ? __ldg(p.bm[l] + r0) : 0;
+  const int64_t w2 = l == L ? __ldg(p.bm[0] + r0) : 0;
+  const int o4 = (int)(w4 & 3), o4c = (int)(w4 & 15), o2 = (int)(w2 & 3);
+  int k4 = 0, k2 = 0;
+  if (l == L) {
+    if (l >= 2) stage_rows<true, true>(own, meta, rank, nch, b, k4, k2, o4, o4c, o2);
+    else stage_rows<false, true>(own, meta, rank, nch, b, k4, k2, o4, o4c, o2);
+  } else {
+    stage_rows<true, false>(own, meta, rank, nch, b, k4, k2, o4, o4c, o2);
+  }
+  __syncwarp();
+  if (k4) {
+    flush_ranks(p.ranks_out[l], w4, b.r4, o4, k4, lane);
+    flush_codes(p.codes_out[l], w4, b.c4, o4c, k4, lane);
+  }
+  if (k2) flush_ranks(p.ranks_out[0], w2, b.r2, o2, k2, lane);
+  __syncwarp();  // the slice is refilled by the next parent
+}
+
+__global__ void __launch_bounds__(kSwThreads)
+    k_lists_write_staged(const __grid_constant__ ListsParams p,
+                         const ListsLayout* __restrict__ glay) {
+  __shared__ ListsLayout lay;
+  extern __shared__ __align__(128) unsigned char sw_smem[];
+  load_layout(glay, lay);
+  __syncthreads();
+  const int L = p.level;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  SwBuf& b = reinterpret_cast<SwBuf*>(sw_smem)[warp];
+  const int64_t nwork = lay.work_off[L + 1];
+  const int64_t gstride = (int64_t)gridDim.x * kSwWarps;
+  for (int64_t gw = (int64_t)blockIdx.x * kSwWarps + warp; gw < nwork; gw += gstride) {
+    int l = lay.lmin;
+    while (lay.work_off[l + 1] <= gw) ++l;
+    const int64_t j = gw - lay.work_off[l];
+    if (l == 0) {
+      if (lane == 0 && p.ktot[0]) p.ranks_out[0][p.bm[0][0]] = 0;
+      continue;
+    }
+    write_parent_staged(p, lay, L, l, j, lane, b);
+  }
+}
+
 // Count + CSR scan in one pass.  A tile is kCsParents consecutive receiver
 // parents P of one level (8 per warp); for each child receiver r of P it
 // counts |E4_l(r)| (and |E2(r)| at l == L) -- lane = window slot, the
