@@ -82,6 +82,11 @@ FMMB_API int64_t fmmb_last_launch_count(fmmb_handle_t h);
  * fmmb_last_sort_path() reports the path the last build completed on (1/2). */
 FMMB_API fmmb_status fmmb_set_sort_path(fmmb_handle_t h, int path);
 FMMB_API int fmmb_last_sort_path(fmmb_handle_t h);
+/* Phase timeline of the last fmmb_build_all when the handle was created with
+ * FMMB_TRACE=1 in the environment (0 entries otherwise): ms[i] since the
+ * build's start event and a static phase name, for up to `cap` boundaries,
+ * recorded on the stream that ran the phase (caller's or side stream). */
+FMMB_API int fmmb_trace(fmmb_handle_t h, float* ms, const char** names, int cap);
 /* Bucket path stream structure: 1 (default) = the local pass and the heads
  * pass run on an internal side stream, concurrently with the directory and
  * the lists on the caller's stream (joined before the call returns);
@@ -157,6 +162,14 @@ FMMB_API fmmb_status fmmb_exclusive_scan_i64(fmmb_handle_t h, const int64_t* val
                                     int64_t n, int64_t* out, int64_t* total,
                                     void* stream);
 
+/* build_bookmarks(bins) (pseudosort.py:68-78): bookmarks (k+1,) = [0,
+ * cumsum(bins[nz])] and the non-empty indices nz (k,) of a dense histogram,
+ * both allocated through `alloc`.  Negative counts raise FMMB_ERR_DOMAIN. */
+FMMB_API fmmb_status fmmb_build_bookmarks(fmmb_handle_t h, const int64_t* bins,
+                                 int64_t nbins, fmmb_alloc_fn alloc, void* ctx,
+                                 int64_t** bookmarks, uint64_t** non_empty,
+                                 int64_t* k, void* stream);
+
 /* --------------------------------------------------------- build API level */
 
 /* One sorted point set, reference layout (pseudosort.py:81-102). */
@@ -218,6 +231,17 @@ FMMB_API fmmb_status fmmb_sort_points(fmmb_handle_t h, const double* points,
                              const double* charges, int64_t n, int level,
                              fmmb_alloc_fn alloc, void* ctx,
                              fmmb_point_set* out, void* stream);
+
+/* reorder(points, charges, bins, boxes, ranks, max_level) (pseudosort.py:
+ * 105-135): permutation[offsets[boxes[i]] + ranks[i]] = i with offsets the
+ * exclusive scan of bins, then points / charges / boxes gathered through it
+ * and the bookmarks of `bins`; every output array allocated through `alloc`.
+ * boxes[i] >= nbins or a position outside [0, n) raise FMMB_ERR_DOMAIN. */
+FMMB_API fmmb_status fmmb_reorder(fmmb_handle_t h, const double* points,
+                         const double* charges, int64_t n, const int64_t* bins,
+                         int64_t nbins, const uint64_t* boxes, const int64_t* ranks,
+                         int level, fmmb_alloc_fn alloc, void* ctx,
+                         fmmb_point_set* out, void* stream);
 
 /* ------------------------------------------- multi-GPU (Morton partition) */
 /* The build of one problem across P GPUs (PAPER.md:923-948,

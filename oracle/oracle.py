@@ -100,6 +100,35 @@ def sort_points(points, charges, level: int) -> SimpleNamespace:
                            bookmarks=bm, non_empty_index=ne, boxes=boxes)
 
 
+def build_bookmarks(bins):
+    """pseudosort.build_bookmarks (pseudosort.py:68-78) via orc_bookmarks."""
+    b = np.ascontiguousarray(bins, dtype=np.int64)
+    bm = np.empty(b.size + 1, dtype=np.int64)
+    ne = np.empty(max(b.size, 1), dtype=np.uint64)
+    k = load().orc_bookmarks(b.ctypes.data, b.size, bm.ctypes.data, ne.ctypes.data)
+    return bm[: k + 1].copy(), ne[:k].copy()
+
+
+def reorder(points, charges, bins, boxes, ranks):
+    """pseudosort.reorder (pseudosort.py:105-135) via orc_reorder + orc_bookmarks."""
+    pts = np.ascontiguousarray(points, dtype=np.float64).reshape(-1, 3)
+    n = pts.shape[0]
+    q = None if charges is None else np.ascontiguousarray(charges, dtype=np.float64)
+    b = np.ascontiguousarray(bins, dtype=np.int64)
+    bx = np.ascontiguousarray(boxes, dtype=np.uint64)
+    rk = np.ascontiguousarray(ranks, dtype=np.int64)
+    pts_out = np.empty_like(pts)
+    q_out = np.empty(n) if q is not None else None
+    perm = np.empty(n, dtype=np.int64)
+    bo = np.empty(n, dtype=np.uint64)
+    load().orc_reorder(_ptr(pts), _ptr(q) if q is not None else None, n, b.ctypes.data, b.size,
+                       _ptr(bx), _ptr(rk), _ptr(pts_out),
+                       _ptr(q_out) if q_out is not None else None, _ptr(perm), _ptr(bo))
+    bm, ne = build_bookmarks(b)
+    return SimpleNamespace(points=pts_out, charges=q_out, permutation=perm, bookmarks=bm,
+                           non_empty_index=ne, boxes=bo)
+
+
 def adjacent_segments(recv, src, level):
     lib = load()
     r = np.ascontiguousarray(recv, dtype=np.uint64)

@@ -60,6 +60,7 @@ SIGNATURES = [
     ("fmmb_set_sort_path", C.c_int, [_p, C.c_int]),
     ("fmmb_last_sort_path", C.c_int, [_p]),
     ("fmmb_set_overlap", C.c_int, [_p, C.c_int]),
+    ("fmmb_trace", C.c_int, [_p, C.POINTER(C.c_float), C.POINTER(C.c_char_p), C.c_int]),
     ("fmmb_spread_bits", C.c_int, [_p, _p, _i64, _p, _p]),
     ("fmmb_compact_bits", C.c_int, [_p, _p, _i64, _p, _p]),
     ("fmmb_interleave_coords", C.c_int, [_p, _p, _p, _p, _i64, _p, _p]),
@@ -73,6 +74,10 @@ SIGNATURES = [
       C.POINTER(_i64), _p]),
     ("fmmb_propagate_to_parents", C.c_int, [_p, _p, _i64, _p, C.POINTER(_i64), _p]),
     ("fmmb_exclusive_scan_i64", C.c_int, [_p, _p, _i64, _p, C.POINTER(_i64), _p]),
+    ("fmmb_build_bookmarks", C.c_int,
+     [_p, _p, _i64, ALLOC_FN, _p, C.POINTER(_p), C.POINTER(_p), C.POINTER(_i64), _p]),
+    ("fmmb_reorder", C.c_int,
+     [_p, _p, _p, _i64, _p, _i64, _p, _p, C.c_int, ALLOC_FN, _p, C.POINTER(PointSetC), _p]),
     ("fmmb_build_all", C.c_int,
      [_p, _p, _p, _i64, _p, _i64, C.c_int, ALLOC_FN, _p, C.POINTER(StructuresC), _p, _p]),
     ("fmmb_sort_points", C.c_int,
@@ -259,3 +264,14 @@ def view(alloc: Allocator, ptr: int | None, count: int, dtype: str, shape=None) 
     if shape is not None:
         t = t.view(*shape)
     return t
+
+
+def trace(dev) -> list[tuple[str, float]]:
+    """(phase, ms since the build's start) of the last build on `dev`
+    (FMMB_TRACE=1 in the environment when the handle was created)."""
+    lib = load()
+    h = handle(dev)
+    ms = (C.c_float * 32)()
+    names = (C.c_char_p * 32)()
+    k = lib.fmmb_trace(h, ms, names, 32)
+    return [(names[i].decode(), float(ms[i])) for i in range(k)]

@@ -56,6 +56,9 @@ struct BucketGeo {
   int64_t n, m;   // sources, receivers
   int cbits;      // bits of a combined input index (n + m <= 2^cbits)
   int hgrid;      // CTAs (histogram rows) of the H pass
+  int qrec;       // source records carry the charge ({x, y, z, q}) and the source
+                  // index goes to the idx side array at the same slot; else the
+                  // record carries the index and k_gather_q sorts the charges
 };
 
 __host__ inline int ceil_log2(int64_t v) {
@@ -97,12 +100,16 @@ __device__ __forceinline__ uint32_t bucket_of(uint64_t key, int is_recv, const B
 // With `fine` non-null (wide geometries, where every non-empty coarse bucket
 // is refined) the same read also counts every point's refinement sub-bin
 // (global atomics into fine[bucket][sub]), so k_bkt_fine's second read of the
-// inputs is skipped.
+// inputs is skipped.  With bmp_src / bmp_recv non-null the pass also sets the
+// level-L occupancy bits, so the directory and the lists can start while the
+// scatter and the local pass still run (build.cu, early occupancy).
 template <bool NARROW>
 __global__ void __launch_bounds__(kHThreads)
     k_bkt_hist(const double* __restrict__ src, const double* __restrict__ recv,
                const BucketGeo g, int level, uint32_t* __restrict__ mat,
-               uint32_t* __restrict__ err, uint32_t* __restrict__ fine) {
+               uint32_t* __restrict__ err, uint32_t* __restrict__ fine,
+               unsigned long long* __restrict__ bmp_src,
+               unsigned long long* __restrict__ bmp_recv) {
   extern __shared__ uint32_t s_hist[];  // [nb]
   const int lane = threadIdx.x & 31;
   for (int b = threadIdx.x; b < g.nb; b += kHThreads) s_hist[b] = 0;
@@ -134,6 +141,11 @@ __global__ void __launch_bounds__(kHThreads)
         bad |= key >= lim;
         const uint32_t b = bucket_of(key & (lim - 1), i >= g.n, g);
         atomicAdd(&s_hist[b], 1u);
+        if (bmp_src) {  // level-L occupancy bit (fire-and-forget reduction)
+          const uint64_t k = key & (lim - 1);
+          unsigned long long* w = (i >= g.n ? bmp_recv : bmp_src) + (k >> 6);
+          asm volatile("red.global.or.b64 [%0], %1;" ::"l"(w), "l"(1ull << (k & 63)) : "memory");
+        }
         if (fine) {
           const int R = g.shift < 8 ? g.shift : 8;  // = ref_bits(g)
           const uint32_t sub = (uint32_t)(((key & (lim - 1)) >> (g.shift - R)) & ((1u << R) - 1u));
@@ -529,6 +541,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
   const double grid = (double)(1ll << level);
   const bool refined = __ldg(fm.maxb) > fm.cap || wide_buckets(g);
   const int R = ref_bits(g);
+  const bool qrec = g.qrec && q != nullptr;
   auto stage_xyz = [&](int k) {
     return reinterpret_cast<double*>(sc_smem + (size_t)(k % kSStages) * kSStageBytes);
   };
@@ -543,6 +556,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
     if (is_src && base + rows > n) return false;  // straddles src | recv
     const double* rp = row_ptr(src, recv, n, base);
     if (((uintptr_t)rp & 15) || ((rows * 24) & 15)) return false;
+    if (is_src && qrec && (((uintptr_t)(q + base) & 15) || ((rows * 8) & 15))) return false;
     return true;
   };
   auto produce = [&](int k) {  // thread 0 only
@@ -552,9 +566,11 @@ __global__ void __launch_bounds__(kSThreads, 1)
       const int64_t base = lo + (int64_t)k * kSRows;
       const int rows = stage_rows(k);
       double* xyz = stage_xyz(k);
+      const bool with_q = base < n && qrec;
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      mbar_expect_tx(full + st, rows * 24);
+      mbar_expect_tx(full + st, rows * 24 + (with_q ? rows * 8 : 0));
       bulk_g2s(xyz, row_ptr(src, recv, n, base), rows * 24, full + st);
+      if (with_q) bulk_g2s(xyz + 3 * kSRows, q + base, rows * 8, full + st);
     } else {
       mbar_arrive(full + st);  // consumers fill this stage themselves
     }
@@ -571,6 +587,7 @@ __global__ void __launch_bounds__(kSThreads, 1)
       xyz[3 * tid] = __ldg(p);
       xyz[3 * tid + 1] = __ldg(p + 1);
       xyz[3 * tid + 2] = __ldg(p + 2);
+      if (qrec && i < n) xyz[3 * kSRows + tid] = __ldg(q + i);
     }
     const uint64_t raw =
         encode_any<NARROW>(xyz[3 * tid], xyz[3 * tid + 1], xyz[3 * tid + 2], level, grid);
@@ -595,10 +612,13 @@ __global__ void __launch_bounds__(kSThreads, 1)
     const double* xyz = stage_xyz(k);
     const int64_t i = lo + (int64_t)k * kSRows + tid;
     if (tid < stage_rows(k) && dst != 0xFFFFFFFFu) {
-      // record = {x, y, z, index within its set}: one 32-B store, no side
-      // array (charges follow the permutation in k_gather_q)
-      const double w = __longlong_as_double(i < n ? i : i - n);
+      // record = {x, y, z, q} + the source index in the side array (qrec), or
+      // {x, y, z, index within its set} (charges then follow the permutation
+      // in k_gather_q): one 32-B store
+      const bool sq = qrec && i < n;
+      const double w = sq ? xyz[3 * kSRows + tid] : __longlong_as_double(i < n ? i : i - n);
       st_v4f64(rec + 4 * (size_t)dst, xyz[3 * tid], xyz[3 * tid + 1], xyz[3 * tid + 2], w);
+      if (sq) idx[dst] = (uint32_t)i;
     }
     mbar_arrive(empty + k % kSStages);
   };
@@ -827,8 +847,12 @@ __global__ void __launch_bounds__(kLcThreads)
   for (int j = tid; j < B; j += kLcThreads) {
     const double* r = s_rec + 4 * j;
     const uint64_t key = encode_any<NARROW>(r[0], r[1], r[2], level, grid);
-    const int64_t li = __double_as_longlong(r[3]);  // index within the set
-    const uint32_t ci = (uint32_t)(set ? n + li : li);  // combined input index
+    // combined input index: source indices from the side array (qrec), else
+    // the record's last word (index within the set)
+    const uint32_t ci = (g.qrec && set == 0)
+                            ? __ldg(idx + rb + j)
+                            : (uint32_t)(set ? n + __double_as_longlong(r[3])
+                                             : __double_as_longlong(r[3]));
     // < span for every valid point; out-of-grid inputs (reported as a DomainError
     // after the build) are clamped so they cannot index outside the bucket
     uint64_t lk = (key & ((1ull << g.sbits) - 1ull)) - prefix;
@@ -931,7 +955,8 @@ __global__ void __launch_bounds__(kLcThreads)
       const int j = p0[pos];
       const double* r = s_rec + 4 * j;
       store_row(o.pts, p, r[0], r[1], r[2]);
-      o.perm[p] = perm_of(o, set, __double_as_longlong(r[3]));
+      o.perm[p] = perm_of(o, set, (int64_t)s_idx[j] - (set ? n : 0));
+      if (g.qrec && set == 0 && o.q) o.q[p] = r[3];
       o.boxes[p] = prefix + (uint64_t)k0[j];
     }
     __syncthreads();  // smem reused by the next bucket
@@ -1007,7 +1032,9 @@ __global__ void __launch_bounds__(kLcThreads)
       const double* r = s_rec + 4 * pl;
       const uint64_t mk = prefix + lk;
       store_row(o.pts, p, r[0], r[1], r[2]);
-      o.perm[p] = perm_of(o, set, __double_as_longlong(r[3]));
+      const int64_t ci = (int64_t)((uint64_t)kc[j] & ((1ull << wb) - 1ull));  // combined index
+      o.perm[p] = perm_of(o, set, ci - (set ? n : 0));
+      if (g.qrec && set == 0 && o.q) o.q[p] = r[3];
       o.boxes[p] = mk;
       const int64_t incl = hbase + woff + __popc(hb & (lt | (1u << lane)));
       if (head) {

@@ -69,8 +69,14 @@ extern "C" fmmb_status fmmb_create(int device, fmmb_handle_t* out) {
   }
   {
     cudaStream_t side;
-    cudaEvent_t e[3];
-    if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaEvent_t e[5];
+    // FMMB_SIDE_PRIO=1: the sort stream at the highest priority, so its
+    // pending CTAs (local pass) are dispatched before the list write's
+    int lo_prio = 0, hi_prio = 0;
+    cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
+    const char* sp = getenv("FMMB_SIDE_PRIO");
+    const int prio = (sp && atoi(sp)) ? hi_prio : 0;
+    if (cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, prio) != cudaSuccess) {
       cudaFreeHost(h->pinned);
       delete h;
       return FMMB_ERR_CUDA;
@@ -80,9 +86,17 @@ extern "C" fmmb_status fmmb_create(int device, fmmb_handle_t* out) {
     h->ev_split = e[0];
     h->ev_rank = e[1];
     h->ev_side = e[2];
+    h->ev_plan = e[3];
+    h->ev_count = e[4];
+    h->scatter_after_count = getenv("FMMB_SCATTER_EARLY") == nullptr;
     h->overlap = getenv("FMMB_NO_OVERLAP") == nullptr;
-    const char* lw = getenv("FMMB_LW");
-    h->list_writer = lw ? atoi(lw) : 1;
+    h->early_occ = getenv("FMMB_LATE_OCC") ? 0 : getenv("FMMB_EARLY_OCC") ? 2 : 1;
+    h->rec_q = getenv("FMMB_REC_IDX") == nullptr;
+    const char* sc = getenv("FMMB_SCATTER_CTAS");
+    h->scatter_ctas = sc ? atoi(sc) : 0;
+    h->trace = getenv("FMMB_TRACE") != nullptr;
+    if (h->trace)
+      for (auto& x : h->tr_ev) cudaEventCreate((cudaEvent_t*)&x);
     h->local_after_count = getenv("FMMB_LOCAL_AFTER") != nullptr;
     const char* lc = getenv("FMMB_LC_PER_SM");
     h->lc_per_sm = lc ? atoi(lc) : 0;
@@ -110,8 +124,6 @@ extern "C" fmmb_status fmmb_create(int device, fmmb_handle_t* out) {
                        (int)scatter_smem_bytes());
   cudaFuncSetAttribute(k_bkt_scatter<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)scatter_smem_bytes());
-  cudaFuncSetAttribute(k_lists_write_staged, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)sw_smem_bytes());
   cudaFuncSetAttribute(k_part_hist, cudaFuncAttributeMaxDynamicSharedMemorySize,
                        (int)(sizeof(uint32_t) << kPartMaxBits));
 #define FMMB_LCATTR(CK, NW, HD)                                                        \
@@ -144,7 +156,9 @@ extern "C" fmmb_status fmmb_destroy(fmmb_handle_t h) {
   cudaSetDevice(h->device);
   if (h->pinned) cudaFreeHost(h->pinned);
   if (h->side) cudaStreamDestroy((cudaStream_t)h->side);
-  for (void* e : {h->ev_split, h->ev_rank, h->ev_side})
+  for (void* e : {h->ev_split, h->ev_rank, h->ev_side, h->ev_plan, h->ev_count})
+    if (e) cudaEventDestroy((cudaEvent_t)e);
+  for (void* e : h->tr_ev)
     if (e) cudaEventDestroy((cudaEvent_t)e);
   delete h;
   return FMMB_OK;
@@ -155,6 +169,26 @@ extern "C" const char* fmmb_last_error(fmmb_handle_t h) {
 }
 
 extern "C" int64_t fmmb_last_launch_count(fmmb_handle_t h) { return h ? h->launches : -1; }
+
+void fmmb_trace_point(fmmb_handle_t h, const char* name, void* stream) {
+  if (!h->trace || h->tr_n >= 32) return;
+  cudaEventRecord((cudaEvent_t)h->tr_ev[h->tr_n], (cudaStream_t)stream);
+  h->tr_name[h->tr_n++] = name;
+}
+
+extern "C" int fmmb_trace(fmmb_handle_t h, float* ms, const char** names, int cap) {
+  if (!h || !h->trace) return 0;
+  FMMB_GUARD(h);
+  const int k = std::min(cap, h->tr_n);
+  for (int i = 0; i < k; ++i) {
+    cudaEventSynchronize((cudaEvent_t)h->tr_ev[i]);
+    float t = 0.f;
+    cudaEventElapsedTime(&t, (cudaEvent_t)h->tr_ev[0], (cudaEvent_t)h->tr_ev[i]);
+    ms[i] = t;
+    names[i] = h->tr_name[i];
+  }
+  return k;
+}
 
 extern "C" fmmb_status fmmb_set_sort_path(fmmb_handle_t h, int path) {
   FMMB_GUARD(h);
@@ -221,6 +255,7 @@ struct BuildPlanHost {  // mirrored in the pinned readback block
 // ---- sort phase, fast path: payload-carrying bucket sort (bucket.cuh)
 struct BucketRun {  // scratch that outlives the sort phase (heads pass)
   std::function<void(cudaStream_t)> local;  // the local pass (+ gid map), launched by the caller
+  std::function<void(cudaStream_t)> scatter;  // deferred scatter (early occupancy), or empty
   char* scratch = nullptr;
   BucketGeo g{};
   const uint32_t* bstart_f = nullptr;
@@ -266,24 +301,48 @@ void launch_spec(const double* src, const double* q, const double* recv, const B
                                                                     ctl + 0, ctl + 2);
 }
 
+// Histogram path.  With `early` the histogram pass (on `s`) also sets the
+// level-L occupancy bits and everything after it (scan, refinement plan,
+// scatter) goes to the sort stream `ss`, split off by ev_split: the caller's
+// stream continues with the directory and the lists while the sort runs.
+// ev_plan (when non-null) marks the plan on `ss`: the refinement overflow
+// flag is final there, long before the scatter ends.
 template <bool NARROW>
 void launch_hs(const double* src, const double* q, const double* recv, const BucketGeo& g,
                int num_sms, int L, uint32_t* mat, uint32_t* bstart, uint64_t* sst, uint32_t* ctl,
                uint32_t* fine, const PlanOut& po, double* rec, uint32_t* idx, uint32_t* err,
-               cudaStream_t s, unsigned long long* const* sbmp) {
+               cudaStream_t s, unsigned long long* const* sbmp, bool early, cudaStream_t ss,
+               cudaEvent_t ev_split, cudaEvent_t ev_plan, int scatter_ctas,
+               std::function<void(cudaStream_t)>* defer_scatter) {
   const bool wide = g.shift > kLcSmallBits;  // every non-empty bucket is refined
   k_bkt_hist<NARROW><<<(unsigned)g.hgrid, kHThreads, (size_t)g.nb * 4, s>>>(
-      src, recv, g, L, mat, err, wide ? fine : nullptr);
-  k_bkt_scan<<<(unsigned)ceil_div(g.nb, kScanBuckets), 256, 0, s>>>(mat, g, bstart, sst,
-                                                                    ctl + 0, ctl + 2);
+      src, recv, g, L, mat, err, wide ? fine : nullptr, early ? sbmp[0] : nullptr,
+      early ? sbmp[1] : nullptr);
+  if (early && ss != s) {
+    cudaEventRecord(ev_split, s);
+    cudaStreamWaitEvent(ss, ev_split, 0);
+  } else {
+    ss = s;
+  }
+  k_bkt_scan<<<(unsigned)ceil_div(g.nb, kScanBuckets), 256, 0, ss>>>(mat, g, bstart, sst,
+                                                                     ctl + 0, ctl + 2);
   if (!wide)
-    k_bkt_fine<NARROW><<<num_sms * 8, 256, 0, s>>>(src, recv, g, L, bstart, ctl + 2, kLcCap,
-                                                   fine);
-  k_bkt_plan<<<(unsigned)ceil_div(g.nb, 256), 256, 0, s>>>(g, bstart, ctl + 2, kLcCap, fine, po);
-  const int sgrid = (int)std::min<int64_t>(num_sms, ceil_div(g.n + g.m, kSRows));
-  const FinalMap fm{po.fbase, po.gtab, ctl + 2, kLcCap, 0u, nullptr, nullptr, {sbmp[0], sbmp[1]}};
-  k_bkt_scatter<NARROW><<<(unsigned)sgrid, kSThreads, scatter_smem_bytes(), s>>>(
-      src, q, recv, g, L, scatter_rows_per_cta(g.n + g.m, sgrid), po.cursor, rec, idx, fm);
+    k_bkt_fine<NARROW><<<num_sms * 8, 256, 0, ss>>>(src, recv, g, L, bstart, ctl + 2, kLcCap,
+                                                    fine);
+  k_bkt_plan<<<(unsigned)ceil_div(g.nb, 256), 256, 0, ss>>>(g, bstart, ctl + 2, kLcCap, fine, po);
+  if (ev_plan) cudaEventRecord(ev_plan, ss);
+  const int sgrid = (int)std::min<int64_t>(std::min(num_sms, std::max(1, scatter_ctas)),
+                                           ceil_div(g.n + g.m, kSRows));
+  const FinalMap fm{po.fbase, po.gtab, ctl + 2, kLcCap, 0u, nullptr, nullptr,
+                    {early ? nullptr : sbmp[0], early ? nullptr : sbmp[1]}};
+  const int64_t rows = scatter_rows_per_cta(g.n + g.m, sgrid);
+  uint32_t* cursor = po.cursor;
+  auto scatter = [=](cudaStream_t st) {
+    k_bkt_scatter<NARROW><<<(unsigned)sgrid, kSThreads, scatter_smem_bytes(), st>>>(
+        src, q, recv, g, L, rows, cursor, rec, idx, fm);
+  };
+  if (defer_scatter) *defer_scatter = scatter;  // launched by the caller (after the list count)
+  else scatter(ss);
 }
 
 // speculative regions apply when the coarse buckets already fit the count path
@@ -303,8 +362,9 @@ inline bool bucket_fits(const BucketGeo& g) { return final_span_bits(g) + g.cbit
 fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int64_t n,
                         const double* recv, int64_t m, int L, const LocalOut& o, bool heads,
                         bool spec, BuildPlanHost* dplan, cudaStream_t s, int64_t& launches,
-                        BucketRun& run, cudaStream_t ls) {
-  const BucketGeo g = bucket_geo(L, n, m, h->num_sms);
+                        BucketRun& run, cudaStream_t ls, bool early) {
+  BucketGeo g = bucket_geo(L, n, m, h->num_sms);
+  g.qrec = (q && n > 0 && h->rec_q) ? 1 : 0;
   const int64_t tot = n + m;
   const int64_t nfcap = final_buckets_cap(g, kLcCap);
   const int64_t nrec = spec ? (int64_t)g.nb * kSpecStride : tot;  // record slots
@@ -357,12 +417,16 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
       launch_spec<false>(src, q, recv, g, h->num_sms, L, mat, bstart, sst, ctl, rbase, po, rec,
                          idx, &dplan->spec_fail, &dplan->err, s, o.bmp);
     po.bstart_f = bstart;
-  } else if (narrow) {
-    launch_hs<true>(src, q, recv, g, h->num_sms, L, mat, bstart, sst, ctl, fine, po, rec, idx,
-                    &dplan->err, s, o.bmp);
   } else {
-    launch_hs<false>(src, q, recv, g, h->num_sms, L, mat, bstart, sst, ctl, fine, po, rec, idx,
-                     &dplan->err, s, o.bmp);
+    cudaEvent_t evs = (cudaEvent_t)h->ev_split, evp = early ? (cudaEvent_t)h->ev_plan : nullptr;
+    const int sc = h->scatter_ctas > 0 ? h->scatter_ctas : h->num_sms;
+    auto* dsc = (early && h->scatter_after_count) ? &run.scatter : nullptr;
+    if (narrow)
+      launch_hs<true>(src, q, recv, g, h->num_sms, L, mat, bstart, sst, ctl, fine, po, rec, idx,
+                      &dplan->err, s, o.bmp, early, ls, evs, evp, sc, dsc);
+    else
+      launch_hs<false>(src, q, recv, g, h->num_sms, L, mat, bstart, sst, ctl, fine, po, rec, idx,
+                       &dplan->err, s, o.bmp, early, ls, evs, evp, sc, dsc);
   }
   // the scatter set the occupancy bits: from here the local pass (on `ls`)
   // and the caller's stream (directory, lists) proceed independently
@@ -393,15 +457,18 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
       else { if (ck32) FMMB_LOCAL(uint32_t, false, false); else FMMB_LOCAL(uint64_t, false, false); }
     }
 #undef FMMB_LOCAL
-    if (q && n > 0 && o.q)
+    fmmb_trace_point(h, "local pass", st);
+    if (q && n > 0 && o.q && !g.qrec)
       k_gather_q<<<(unsigned)h->num_sms * 16, 256, 0, st>>>(o.perm, q, n, o.q, lfail);
     if (o.gid[0] || o.gid[1])
       k_gid_map<<<(unsigned)h->num_sms * 16, 256, 0, st>>>(o.perm, n, m, o.gid[0], o.gid[1],
                                                             lfail);
+    fmmb_trace_point(h, "charge gather", st);
   };
   // spec: init, scatter, counts, scan; hist: hist, scan, [fine], plan, scatter; + local
   const int sort_kernels = spec ? 4 : (g.shift > kLcSmallBits ? 4 : 5);
-  launches += sort_kernels + 1 + ((o.gid[0] || o.gid[1]) ? 1 : 0) + ((q && n > 0 && o.q) ? 1 : 0);
+  launches += sort_kernels + 1 + ((o.gid[0] || o.gid[1]) ? 1 : 0) +
+              ((q && n > 0 && o.q && !g.qrec) ? 1 : 0);
   run.local = local;
   run.scratch = w;
   run.g = g;
@@ -466,22 +533,12 @@ fmmb_status sort_onesweep(fmmb_handle_t h, const double* src, const double* q, i
   return FMMB_OK;
 }
 
-// E2/E4 write pass: the staged writer (per-parent shared-memory compaction,
-// 32-B vector stores) unless FMMB_LW=0 selects the per-lane-store writer
+// E2/E4 write pass (warp per receiver parent, grid-stride)
 inline void launch_lists_write(fmmb_handle_t h, const ListsParams& lp, const ListsLayout* lay,
                                int64_t nwork_cap, cudaStream_t s) {
-  if (h->list_writer == 0) {
-    const int lgrid = (int)std::max<int64_t>(
-        1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * 16));
-    k_lists_write<<<lgrid, kLThreads, 0, s>>>(lp, lay);
-    return;
-  }
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_lists_write_staged, kSwThreads,
-                                                sw_smem_bytes());
   const int lgrid = (int)std::max<int64_t>(
-      1, std::min<int64_t>(ceil_div(nwork_cap, kSwWarps), (int64_t)h->num_sms * std::max(per_sm, 1)));
-  k_lists_write_staged<<<lgrid, kSwThreads, sw_smem_bytes(), s>>>(lp, lay);
+      1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * 16));
+  k_lists_write<<<lgrid, kLThreads, 0, s>>>(lp, lay);
 }
 
 // Multi-GPU sort phase extras: global indices of the local points and the
@@ -604,6 +661,8 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     if (ls != s) cudaStreamWaitEvent(s, (cudaEvent_t)h->ev_side, 0);
   };
   for (int attempt = 0;; ++attempt) {
+    h->tr_n = 0;
+    fmmb_trace_point(h, "start", s);
     if (ev) cudaEventRecord(ev[0], s);
     cudaMemsetAsync(ws, 0, zero_bytes, s);
     if (tot == 0) cudaMemsetAsync(bm_out, 0, 2 * sizeof(int64_t), s);
@@ -611,10 +670,19 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     // ---- K1-K4: sort both sets into the reference layout
     BucketRun brun;
     ls = (fast && heads && h->overlap && h->side) ? (cudaStream_t)h->side : s;
+    // early occupancy: the histogram pass sets the level-L bits and the sort
+    // continues on the side stream while this stream builds the directory
+    // and the lists (which need nothing but the bitmaps)
+    // (chosen when the histogram pass runs anyway -- wide or skewed
+    // geometries, c3: measured 3.57 vs 3.71 ms; with speculative regions
+    // the scatter sets the bits itself -- c2: 3.04 vs 3.19 ms)
+    const bool early = fast && lists && !dsa && ls != s &&
+                       (h->early_occ == 2 || (h->early_occ == 1 && !spec));
+    if (early) spec = false;
     if (tot > 0) {
       const fmmb_status st =
           fast ? sort_bucket(h, src, q, n, recv, m, L, lo, heads, spec, dplan, s, launches, brun,
-                             ls)
+                             ls, early)
                : sort_onesweep<KeyT>(h, src, q, n, recv, m, L, lo, dplan, s, launches);
       if (st != FMMB_OK) {
         join();
@@ -627,14 +695,16 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     // when h->local_after_count (A/B knob FMMB_LOCAL_AFTER=1)
     auto start_local = [&]() {
       if (!brun.local) return;
-      if (ls != s) {
+      if (ls != s && !early) {  // (early: the scatter already runs on ls)
         cudaEventRecord((cudaEvent_t)h->ev_split, s);
         cudaStreamWaitEvent(ls, (cudaEvent_t)h->ev_split, 0);
       }
       brun.local(ls);
       brun.local = nullptr;
     };
-    if (!h->local_after_count || !lists) start_local();
+    fmmb_trace_point(h, early ? "hist+occupancy (s)" : "sort (s)", s);
+    if (early && !brun.scatter) fmmb_trace_point(h, "scan+plan+scatter (side)", ls);
+    if ((!h->local_after_count || !lists) && !brun.scatter) start_local();
     if (ev) cudaEventRecord(ev[1], s);
 
     // ---- K5: bitmap pyramid (big levels one launch each, the rest in one CTA)
@@ -679,6 +749,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
       k_rank<<<(unsigned)rank_tiles, kRThreads, 0, s>>>(rp);
       ++launches;
     }
+    fmmb_trace_point(h, "pyramid+rank (s)", s);
     if (dsa && dsa->bmp) {  // this rank's level-L occupancy, for the all-reduce
       cudaMemcpyAsync(dsa->bmp, bmp + rp.word_off[L], level_words(L) * sizeof(uint64_t),
                       cudaMemcpyDeviceToDevice, s);
@@ -706,9 +777,17 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
           1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * 16));
       ListsLayout* glay = (ListsLayout*)W(o_lay);
       k_lists_plan<<<1, 32, 0, s>>>(lp, glay);
-      k_lists_cscan<false><<<(unsigned)cs_tiles, kLThreads, 0, s>>>(
+      k_lists_cscan<<<(unsigned)cs_tiles, kLThreads, 0, s>>>(
           lp, glay, (uint64_t*)W(o_st4), (uint64_t*)W(o_st2), tc + 10, dplan->seg_totals);
       launches += 2;
+      fmmb_trace_point(h, "lists count (s)", s);
+    }
+    if (brun.scatter) {  // early occupancy: the scatter starts once the count has its SMs
+      cudaEventRecord((cudaEvent_t)h->ev_count, s);
+      cudaStreamWaitEvent(ls, (cudaEvent_t)h->ev_count, 0);
+      brun.scatter(ls);
+      brun.scatter = nullptr;
+      fmmb_trace_point(h, "scatter (side)", ls);
     }
     start_local();
     if (brun.scratch) {  // bucket path: bookmarks / non-empty keys at global box ranks
@@ -733,14 +812,18 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
         k_bkt_heads<<<(unsigned)h->num_sms * 8, 256, 0, ls>>>(hpar, brun.desc, brun.nfinal,
                                                                brun.g);
         ++launches;
+        fmmb_trace_point(h, ls != s ? "heads (side)" : "heads (s)", ls);
       }
       cudaFreeAsync(brun.scratch, ls);
     }
     if (ls != s) cudaEventRecord((cudaEvent_t)h->ev_side, ls);
     if (ev) cudaEventRecord(ev[3], s);
 
-    // ---- sizes back to the host (the build's single synchronisation)
+    // ---- sizes back to the host (the build's single synchronisation); early
+    // occupancy: the sort stream's refinement plan (overflow flag) first
+    if (early && tot > 0) cudaStreamWaitEvent(s, (cudaEvent_t)h->ev_plan, 0);
     cudaMemcpyAsync(hp, dplan, sizeof(BuildPlanHost), cudaMemcpyDeviceToHost, s);
+    fmmb_trace_point(h, "size read-back (s)", s);
     cudaError_t ce = cudaStreamSynchronize(s);
     if (ce != cudaSuccess) {
       join();
@@ -830,8 +913,10 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
       lp.codes_out[k] = (int16_t*)(arena_b + b_c[k]);
     }
     if (ev) cudaEventRecord(ev[4], s);
+    fmmb_trace_point(h, "host: list arena (s)", s);
     launch_lists_write(h, lp, (const ListsLayout*)W(o_lay), nwork_cap, s);
     ++launches;
+    fmmb_trace_point(h, "lists write (s)", s);
     if (ev) cudaEventRecord(ev[5], s);  // the write kernel alone (before the side join)
 
     out->neighbor_bookmark = lp.bm[0];
@@ -855,6 +940,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     }
   }
   join();  // the caller's stream sees the local pass and heads complete
+  fmmb_trace_point(h, "joined (s)", s);
   if (ev) {
     if (!lists) {
       cudaEventRecord(ev[4], s);

@@ -24,10 +24,26 @@ struct fmmb_handle_s {
   void* ev_split = nullptr;      // cudaEvent_t: scatter done (caller stream)
   void* ev_rank = nullptr;       // rank directory done (caller stream)
   void* ev_side = nullptr;       // side stream's work done
+  void* ev_plan = nullptr;       // early occupancy: refinement plan done (sort stream)
+  void* ev_count = nullptr;      // early occupancy: list count done (caller stream)
+  bool scatter_after_count = true;  // early occupancy: scatter waits for the list count
+                                    // (FMMB_SCATTER_EARLY=1: right after the plan)
+  int early_occ = 1;             // occupancy bits from the histogram pass, sort on the side
+                                 // stream beside the directory + lists: 1 when the histogram
+                                 // pass runs anyway, 2 always (FMMB_EARLY_OCC=1), 0 never
+                                 // (FMMB_LATE_OCC=1)
+  bool rec_q = true;             // source records carry q + idx side store (FMMB_REC_IDX=1:
+                                 // records carry the index, charges gathered after the sort)
+  int scatter_ctas = 0;          // FMMB_SCATTER_CTAS: cap on the scatter's persistent grid (A/B)
   bool overlap = true;           // FMMB_NO_OVERLAP=1 serialises (A/B)
   bool local_after_count = false;  // FMMB_LOCAL_AFTER=1: local pass after the list count (A/B)
   int lc_per_sm = 0;             // FMMB_LC_PER_SM: cap on resident local-pass CTAs per SM (A/B)
-  int list_writer = 1;           // 1 staged (default), 0 per-lane stores (FMMB_LW=0, A/B)
+  // FMMB_TRACE=1: timing events at the phase boundaries of both streams of
+  // the last build (fmmb_trace): the overlap timeline without a profiler
+  bool trace = false;
+  int tr_n = 0;
+  void* tr_ev[32] = {};
+  const char* tr_name[32] = {};
   // every entry point holds this for its whole call: the pinned read-back
   // block, the side stream and its events are per handle, so concurrent
   // callers on one device (the reference's kernels are nogil and reentrant,
@@ -45,3 +61,4 @@ constexpr size_t kPinnedBytes = 1 << 16;
 fmmb_status fmmb_fail(fmmb_handle_t h, fmmb_status st, const char* fmt, ...);
 bool fmmb_bitmap_ok(int level, int64_t n_total);
 int lists_lmin_host(int L);
+void fmmb_trace_point(fmmb_handle_t h, const char* name, void* stream);

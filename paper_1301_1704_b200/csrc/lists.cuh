@@ -231,286 +231,190 @@ __device__ __forceinline__ void st_rank_code(unsigned pred, int64_t* r, int64_t 
       "l"(r), "l"(rank), "l"(c), "h"((short)code)
       : "memory");
 }
+__device__ __forceinline__ void st_code(unsigned pred, int16_t* c, int code) {
+  asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.global.s16 [%1], %2;\n\t}" ::
+                   "r"(pred), "l"(c), "h"((short)code)
+               : "memory");
+}
 __device__ __forceinline__ void st_rank(unsigned pred, int64_t* r, int64_t rank) {
   asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.u32 p, %0, 0;\n\t@p st.global.s64 [%1], %2;\n\t}" ::
                    "r"(pred), "l"(r), "l"(rank)
                : "memory");
 }
 
+// ---- window order without a sort network.  The Morton order of the 27
+// members (x+dx, y+dy, z+dz) of P's window is decided, for a pair of members,
+// by the axis with the highest (h * 3 + axis), h = highest differing bit of
+// the two coordinates: h(x-1, x) = ctz(x), h(x, x+1) = ctz(x+1) and h(x-1,
+// x+1) = the larger of the two.  One of ctz(x), ctz(x+1) is 0, so an axis
+// is described by its parity and one level K >= 1, and the whole order by
+// the three parities and the ranking of (K_a * 3 + a): 8 x 6 = 48 cases,
+// tabulated at compile time from one representative each (members outside
+// the grid keep their place and are skipped: no children).
+__host__ __device__ constexpr uint64_t cx_morton3(uint64_t x, uint64_t y, uint64_t z) {
+  uint64_t k = 0;
+  for (int b = 0; b < 21; ++b)
+    k |= (((x >> b) & 1ull) << (3 * b)) | (((y >> b) & 1ull) << (3 * b + 1)) |
+         (((z >> b) & 1ull) << (3 * b + 2));
+  return k;
+}
+struct WinOrder {
+  uint8_t o[48][32];  // [case][sorted position] = window offset (27 = unused)
+  constexpr WinOrder() : o() {
+    constexpr int ranks[6][3] = {{0, 1, 2}, {0, 2, 1}, {1, 0, 2}, {1, 2, 0}, {2, 0, 1}, {2, 1, 0}};
+    for (int cs = 0; cs < 48; ++cs) {
+      uint64_t c[3] = {0, 0, 0};
+      for (int a = 0; a < 3; ++a) {
+        const int K = ranks[cs >> 3][a] + 1;
+        c[a] = ((cs >> a) & 1) ? (3ull << K) - 1 : (3ull << K);
+      }
+      uint64_t key[27] = {};
+      int idx[27] = {};
+      for (int q = 0; q < 27; ++q) {
+        key[q] = cx_morton3(c[0] + q % 3 - 1, c[1] + (q / 3) % 3 - 1, c[2] + q / 9 - 1);
+        idx[q] = q;
+      }
+      for (int i = 0; i < 27; ++i)  // selection sort (compile time)
+        for (int j = i + 1; j < 27; ++j)
+          if (key[idx[j]] < key[idx[i]]) {
+            const int t = idx[i];
+            idx[i] = idx[j];
+            idx[j] = t;
+          }
+      for (int i = 0; i < 32; ++i) o[cs][i] = (uint8_t)(i < 27 ? idx[i] : 27);
+    }
+  }
+};
+__constant__ WinOrder kWinOrder = WinOrder();
+
+// case of parent P (level l1 >= 0): parities | ranking of (K_a * 3 + a) << 3
+__device__ __forceinline__ int window_case(uint64_t P, int l1) {
+  const int bits = 3 * l1;
+  const uint64_t full = bits >= 64 ? ~0ull : ((1ull << bits) - 1ull);
+  int par = 0, kk[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const uint64_t m = (kDilated << a) & full;
+    const uint64_t xa = P & m;
+    const int odd = (int)((xa >> a) & 1ull);
+    const uint64_t v = odd ? ((((P | ~m) + 1ull) & m)) : xa;  // dilated x+1 or x
+    const int K = v ? (__ffsll((long long)v) - 1 - a) / 3 : 64;
+    par |= odd << a;
+    kk[a] = K * 3 + a;
+  }
+  const int rx = (kk[0] > kk[1]) + (kk[0] > kk[2]);
+  const int ry = (kk[1] > kk[0]) + (kk[1] > kk[2]);
+  // (rx, ry) -> index of the ranking in WinOrder's table
+  const int pi = rx == 0 ? (ry == 1 ? 0 : 1) : rx == 1 ? (ry == 0 ? 2 : 3) : (ry == 0 ? 4 : 5);
+  return par | (pi << 3);
+}
+
+// per (window offset o, candidate child c): bits 0-7 near-over-cr (child c of
+// o is in the 3x3x3 window of child receiver cr), bits 8+ the E4 code base
+// 2*(ox + 7 oy + 49 oz) + (c_x + 7 c_y + 49 c_z) + 171 (minus the receiver's
+// own child offset later); o = 27 (unused lanes) is all zero
+struct CandTable {
+  uint32_t v[28 * 8];
+  constexpr CandTable() : v() {
+    for (int o = 0; o < 27; ++o) {
+      const int off[3] = {o % 3 - 1, (o / 3) % 3 - 1, o / 9 - 1};
+      for (int c = 0; c < 8; ++c) {
+        uint32_t near = 0;
+        for (int cr = 0; cr < 8; ++cr) {
+          bool in = true;
+          for (int a = 0; a < 3; ++a) {
+            const int d = 2 * off[a] + ((c >> a) & 1) - ((cr >> a) & 1);
+            in = in && d >= -1 && d <= 1;
+          }
+          if (in) near |= 1u << cr;
+        }
+        const int code = 2 * off[0] + 14 * off[1] + 98 * off[2] + (c & 1) + 7 * ((c >> 1) & 1) +
+                         49 * ((c >> 2) & 1) + 171;
+        v[o * 8 + c] = near | ((uint32_t)code << 8);
+      }
+    }
+  }
+};
+__constant__ CandTable kCand = CandTable();
+
+struct ListsSmem {  // per-CTA copies of the tables (lane-divergent lookups)
+  uint8_t order[48][32];
+  uint32_t cand[28 * 8];
+};
+__device__ __forceinline__ void load_tables(ListsSmem& t) {
+  for (int i = threadIdx.x; i < 48 * 32 / 4; i += blockDim.x)
+    reinterpret_cast<uint32_t*>(&t.order[0][0])[i] =
+        reinterpret_cast<const uint32_t*>(&kWinOrder.o[0][0])[i];
+  for (int i = threadIdx.x; i < 28 * 8; i += blockDim.x) t.cand[i] = kCand.v[i];
+}
+
+// Rows of the owned child receivers (bits of rm, ascending = row order).
+// Chunk ch (32 candidates) of row cr: occupied candidates split into E2
+// (near cr) and E4 (the rest); both positions come from one ballot of the
+// near-and-occupied lanes and the chunk's occupied prefix (shared by the
+// rows), and every occupied lane issues ONE rank store (to E2 or E4).
 template <bool E4, bool E2>
 __device__ __forceinline__ void write_rows(uint32_t rm, const uint32_t (&meta)[7],
                                            const uint32_t (&rank)[7], int64_t* __restrict__ r4,
                                            int16_t* __restrict__ c4, int64_t* __restrict__ r2) {
   const unsigned lt = lanemask_lt();
+  uint32_t occ_lt[7], occ_n[7];
+#pragma unroll
+  for (int ch = 0; ch < 7; ++ch) {
+    const unsigned ob = ballot_full(meta[ch] & 1u);
+    occ_lt[ch] = __popc(ob & lt);
+    occ_n[ch] = __popc(ob);
+  }
   uint32_t rbits = rm;
   while (rbits) {
     const int cr = __ffs(rbits) - 1;
     rbits &= rbits - 1;
     const int crw = (cr & 1) + 7 * ((cr >> 1) & 1) + 49 * ((cr >> 2) & 1);
-    const int sh = 1 + cr;
 #pragma unroll
     for (int ch = 0; ch < 7; ++ch) {
       const uint32_t m = meta[ch];
-      const uint32_t nb = m >> sh;
+      const uint32_t occ = m & 1u;
+      const uint32_t near = (m >> (1 + cr)) & occ;
+      const unsigned nb = ballot_full(near);
+      const uint32_t a2 = __popc(nb & lt), n2 = __popc(nb);
+      const uint32_t a4 = occ_lt[ch] - a2, n4 = occ_n[ch] - n2;
+      if (E2 && E4) {
+        int64_t* dst = near ? r2 + a2 : r4 + a4;
+        st_rank(occ, dst, (int64_t)rank[ch]);
+        st_code(occ & ~near, c4 + a4, (int)(m >> 9) - crw);
+      } else if (E4) {
+        st_rank_code(occ & ~near, r4 + a4, (int64_t)rank[ch], c4 + a4, (int)(m >> 9) - crw);
+      } else {
+        st_rank(near, r2 + a2, (int64_t)rank[ch]);
+      }
       if (E4) {
-        const unsigned v = m & ~nb & 1u;
-        const unsigned b = ballot_full(v);
-        const unsigned at = __popc(b & lt);
-        st_rank_code(v, r4 + at, (int64_t)rank[ch], c4 + at, (int)(m >> 9) - crw);
-        r4 += __popc(b);
-        c4 += __popc(b);
+        r4 += n4;
+        c4 += n4;
       }
-      if (E2) {
-        const unsigned v = m & nb & 1u;
-        const unsigned b = ballot_full(v);
-        st_rank(v, r2 + __popc(b & lt), (int64_t)rank[ch]);
-        r2 += __popc(b);
-      }
+      if (E2) r2 += n2;
     }
   }
 }
 
 // One receiver parent P (level l-1, rank j among the work parents of level
-// l): its rows of E4 (and E2 at l == L).  FRESH: the bookmarks were written
-// by this kernel (read through L2, not the read-only path).
-template <bool FRESH>
+// l): its rows of E4 (and E2 at l == L).  Lane s holds the s-th window
+// member in key order (table, no sort); chunk ch covers members 4ch..4ch+3
+// (lane / 8) and their 8 children (lane % 8): occupancy, source rank, the
+// near bits over the 8 child receivers and the code base, once per P.
 __device__ __forceinline__ void write_parent(const ListsParams& p, const ListsLayout& lay,
-                                             int L, int l, int64_t j, int lane) {
+                                             const ListsSmem& t, int L, int l, int64_t j,
+                                             int lane) {
   const unsigned FULL = 0xffffffffu;
   const int c = lane & 7;
-  // code contribution of the candidate child c: (c_x + 7 c_y + 49 c_z) + 3*57
-  const int cc = (c & 1) + 7 * ((c >> 1) & 1) + 49 * ((c >> 2) & 1) + 171;
   const uint64_t P = __ldg(p.rkeys[l - 1] + lay.p_lo[l] + j);
-  uint64_t qk = window_key(P, l, lane);
-  int o = lane;
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-    for (int d = k >> 1; d > 0; d >>= 1) {
-      const uint64_t ok = __shfl_xor_sync(FULL, qk, d);
-      const int oo = __shfl_xor_sync(FULL, o, d);
-      const bool want_min = ((lane & d) == 0) == ((lane & k) == 0);
-      if (want_min ? (ok < qk) : (ok > qk)) {
-        qk = ok;
-        o = oo;
-      }
-    }
-  }
+  const int o = t.order[window_case(P, l - 1)][lane];
+  const uint64_t qk = window_key(P, l, o);
   uint32_t sm = 0, sfirst = 0;
   if (qk != ~0ull)
     children_of(p.bmp + p.bmp_off[0][l], p.dir + p.bmp_off[0][l], qk, sm, sfirst);
   uint32_t rm, rfirst;
   children_of(p.bmp + p.bmp_off[1][l], p.dir + p.bmp_off[1][l], P, rm, rfirst);
-  // per chunk: meta = occ | near-over-cr (8 bits) << 1 | code base << 9
-  const uint32_t slot_word = sm | ((uint32_t)(o < 27 ? o : 13) << 8);
-  uint32_t meta[7], rank[7];
-#pragma unroll
-  for (int ch = 0; ch < 7; ++ch) {
-    const int slot = 4 * ch + (lane >> 3);
-    const uint32_t v = __shfl_sync(FULL, slot_word, slot);
-    const uint32_t f = __shfl_sync(FULL, sfirst, slot);
-    const uint32_t smk = v & 0xFFu;
-    const int so = (int)(v >> 8);
-    const uint64_t nw = kNear.w[so];
-    uint32_t nearcr = 0;
-#pragma unroll
-    for (int cr = 0; cr < 8; ++cr) nearcr |= ((uint32_t)(nw >> (8 * cr + c)) & 1u) << cr;
-    const int sx = so % 3 - 1, sy = (so / 3) % 3 - 1, sz = so / 9 - 1;
-    const uint32_t code0 = (uint32_t)(2 * sx + 7 * 2 * sy + 49 * 2 * sz + cc);
-    const bool occ = slot < 27 && ((smk >> c) & 1u);
-    meta[ch] = (occ ? 1u : 0u) | (nearcr << 1) | (code0 << 9);
-    rank[ch] = f + __popc(smk & ((1u << c) - 1u));
-  }
-  int64_t* r4 = p.ranks_out[l];
-  int16_t* c4 = p.codes_out[l];
-  int64_t* r2 = p.ranks_out[0];
   // owned children (a contiguous run of ranks) and the first one's CSR row
-  uint32_t own = 0;
-  int64_t r0 = -1;
-  {
-    int64_t r = rfirst;
-#pragma unroll
-    for (int c = 0; c < 8; ++c)
-      if ((rm >> c) & 1u) {
-        if (r >= lay.r_lo[l] && r < lay.r_hi[l]) {
-          own |= 1u << c;
-          if (r0 < 0) r0 = r - lay.r_lo[l];
-        }
-        ++r;
-      }
-  }
-  rm = own;
-  if (!rm) return;
-  rfirst = (uint32_t)r0;
-  if (l == L) {
-    const int64_t w2 = FRESH ? __ldcg(p.bm[0] + rfirst) : __ldg(p.bm[0] + rfirst);
-    if (l >= 2) {
-      const int64_t w4 = FRESH ? __ldcg(p.bm[l] + rfirst) : __ldg(p.bm[l] + rfirst);
-      write_rows<true, true>(rm, meta, rank, r4 + w4, c4 + w4, r2 + w2);
-    } else {
-      write_rows<false, true>(rm, meta, rank, nullptr, nullptr, r2 + w2);
-    }
-  } else {
-    const int64_t w4 = FRESH ? __ldcg(p.bm[l] + rfirst) : __ldg(p.bm[l] + rfirst);
-    write_rows<true, false>(rm, meta, rank, r4 + w4, c4 + w4, nullptr);
-  }
-}
-
-__global__ void __launch_bounds__(kLThreads)
-    k_lists_write(const __grid_constant__ ListsParams p, const ListsLayout* __restrict__ glay) {
-  __shared__ ListsLayout lay;
-  load_layout(glay, lay);
-  __syncthreads();
-  const int L = p.level;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t nwork = lay.work_off[L + 1];
-  const int64_t gstride = (int64_t)gridDim.x * kLWarps;
-  for (int64_t gw = (int64_t)blockIdx.x * kLWarps + warp; gw < nwork; gw += gstride) {
-    int l = lay.lmin;
-    while (lay.work_off[l + 1] <= gw) ++l;
-    const int64_t j = gw - lay.work_off[l];
-    if (l == 0) {
-      if (lane == 0 && p.ktot[0]) p.ranks_out[0][p.bm[0][0]] = 0;
-      continue;
-    }
-    write_parent<false>(p, lay, L, l, j, lane);
-  }
-}
-
-// ------------------------------------------------------ staged write ----
-// Write pass, staged: a warp compacts ALL rows of its receiver parent P (the
-// owned child rows are consecutive in every CSR, so P's E4 entries, codes
-// and E2 entries are three contiguous output ranges) into its shared-memory
-// slice -- u32 ranks (box ranks < 2^31), i16 codes -- and then streams each
-// range out as 32-byte aligned vector stores (lane = one 32-B unit, a warp
-// store = 1 KB of full L2 lines); only the unaligned first / last unit of a
-// range is stored element-wise.  Same enumeration and ballot compaction as
-// write_rows, but the compaction targets shared memory, so HBM sees full-line
-// writes instead of per-lane 8-B / 2-B stores at arbitrary alignment.
-#ifndef FMMB_SWWARPS
-#define FMMB_SWWARPS 8
-#endif
-constexpr int kSwWarps = FMMB_SWWARPS;
-constexpr int kSwThreads = kSwWarps * 32;
-constexpr int kSwE4 = 8 * 189;  // an E4 row holds <= 216 - 27 entries
-constexpr int kSwE2 = 8 * 27;
-struct __align__(32) SwBuf {
-  uint32_t r4[kSwE4 + 8];
-  uint32_t r2[kSwE2 + 8];
-  int16_t c4[kSwE4 + 32];
-  uint32_t slot_word[32];  // occupied window slots, compacted in key order
-  uint32_t slot_first[32];
-};
-__host__ __device__ constexpr size_t sw_smem_bytes() { return sizeof(SwBuf) * kSwWarps; }
-
-__device__ __forceinline__ void st_v4_b64(void* p, uint64_t a, uint64_t b, uint64_t c,
-                                          uint64_t d) {
-#ifdef FMMB_LW_CS
-  asm volatile("st.global.cs.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c),
-               "l"(d)
-               : "memory");
-#else
-  asm volatile("st.global.v4.b64 [%0], {%1, %2, %3, %4};" ::"l"(p), "l"(a), "l"(b), "l"(c),
-               "l"(d)
-               : "memory");
-#endif
-}
-
-template <bool E4, bool E2>
-__device__ __forceinline__ void stage_rows(uint32_t rm, const uint32_t (&meta)[7],
-                                           const uint32_t (&rank)[7], int nch, SwBuf& b,
-                                           int& k4, int& k2, int o4, int o4c, int o2) {
-  const unsigned lt = lanemask_lt();
-  uint32_t rbits = rm;
-  while (rbits) {
-    const int cr = __ffs(rbits) - 1;
-    rbits &= rbits - 1;
-    const int crw = (cr & 1) + 7 * ((cr >> 1) & 1) + 49 * ((cr >> 2) & 1);
-    const int sh = 1 + cr;
-#pragma unroll
-    for (int ch = 0; ch < 7; ++ch) {
-      if (ch >= nch) break;  // warp-uniform: only chunks holding occupied slots
-      const uint32_t m = meta[ch];
-      const uint32_t nb = m >> sh;
-      if (E4) {
-        const unsigned v = m & ~nb & 1u;
-        const unsigned bl = ballot_full(v);
-        if (v) {
-          const int at = k4 + __popc(bl & lt);
-          b.r4[o4 + at] = rank[ch];
-          b.c4[o4c + at] = (int16_t)((int)(m >> 9) - crw);
-        }
-        k4 += __popc(bl);
-      }
-      if (E2) {
-        const unsigned v = m & nb & 1u;
-        const unsigned bl = ballot_full(v);
-        if (v) b.r2[o2 + k2 + __popc(bl & lt)] = rank[ch];
-        k2 += __popc(bl);
-      }
-    }
-  }
-}
-
-// s[o + k] -> g[w + k] for k < T (u32 -> i64); g + (w - o) is 32-B aligned
-__device__ __forceinline__ void flush_ranks(int64_t* __restrict__ g, int64_t w,
-                                            const uint32_t* s, int o, int T, int lane) {
-  int64_t* g0 = g + (w - o);
-  const int end = o + T;
-  for (int i0 = 4 * lane; i0 < end; i0 += 128) {
-    if (i0 >= o && i0 + 4 <= end) {
-      const uint4 v = *reinterpret_cast<const uint4*>(s + i0);
-      st_v4_b64(g0 + i0, v.x, v.y, v.z, v.w);
-    } else {
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (i0 + j >= o && i0 + j < end) g0[i0 + j] = (int64_t)s[i0 + j];
-    }
-  }
-}
-
-// codes: 16 per 32-B unit
-__device__ __forceinline__ void flush_codes(int16_t* __restrict__ g, int64_t w, const int16_t* s,
-                                            int o, int T, int lane) {
-  int16_t* g0 = g + (w - o);
-  const int end = o + T;
-  for (int i0 = 16 * lane; i0 < end; i0 += 512) {
-    if (i0 >= o && i0 + 16 <= end) {
-      const ulonglong4 v = *reinterpret_cast<const ulonglong4*>(s + i0);
-      st_v4_b64(g0 + i0, v.x, v.y, v.z, v.w);
-    } else {
-      for (int j = 0; j < 16; ++j)
-        if (i0 + j >= o && i0 + j < end) g0[i0 + j] = s[i0 + j];
-    }
-  }
-}
-
-__device__ __forceinline__ void write_parent_staged(const ListsParams& p, const ListsLayout& lay,
-                                                    int L, int l, int64_t j, int lane, SwBuf& b) {
-  const unsigned FULL = 0xffffffffu;
-  const int c = lane & 7;
-  const int cc = (c & 1) + 7 * ((c >> 1) & 1) + 49 * ((c >> 2) & 1) + 171;
-  const uint64_t P = __ldg(p.rkeys[l - 1] + lay.p_lo[l] + j);
-  uint64_t qk = window_key(P, l, lane);
-  int o = lane;
-#pragma unroll
-  for (int k = 2; k <= 32; k <<= 1) {
-#pragma unroll
-    for (int d = k >> 1; d > 0; d >>= 1) {
-      const uint64_t ok = __shfl_xor_sync(FULL, qk, d);
-      const int oo = __shfl_xor_sync(FULL, o, d);
-      const bool want_min = ((lane & d) == 0) == ((lane & k) == 0);
-      if (want_min ? (ok < qk) : (ok > qk)) {
-        qk = ok;
-        o = oo;
-      }
-    }
-  }
-  uint32_t sm = 0, sfirst = 0;
-  if (qk != ~0ull)
-    children_of(p.bmp + p.bmp_off[0][l], p.dir + p.bmp_off[0][l], qk, sm, sfirst);
-  uint32_t rm, rfirst;
-  children_of(p.bmp + p.bmp_off[1][l], p.dir + p.bmp_off[1][l], P, rm, rfirst);
   uint32_t own = 0;
   int64_t r0 = -1;
   {
@@ -526,68 +430,53 @@ __device__ __forceinline__ void write_parent_staged(const ListsParams& p, const 
       }
   }
   if (!own) return;
-  // occupied window slots (source children present), compacted in key order:
-  // candidate chunk ch covers compacted slots 4ch..4ch+3, so sparse windows
-  // (surfaces, deep levels) visit ceil(slots / 4) chunks instead of 7
-  const unsigned occ_slots = __ballot_sync(FULL, sm != 0u);
-  const int nslot = __popc(occ_slots);
-  if (sm) {
-    const int at = __popc(occ_slots & lanemask_lt());
-    b.slot_word[at] = sm | ((uint32_t)o << 8);
-    b.slot_first[at] = sfirst;
-  }
-  __syncwarp();
-  const int nch = (nslot + 3) >> 2;
+  // per chunk: meta = occ | near-over-cr (8 bits) << 1 | code base << 9
+  const uint32_t slot_word = sm | ((uint32_t)o << 8);
   uint32_t meta[7], rank[7];
 #pragma unroll
   for (int ch = 0; ch < 7; ++ch) {
     const int slot = 4 * ch + (lane >> 3);
-    const uint32_t v = slot < nslot ? b.slot_word[slot] : (13u << 8);
-    const uint32_t f = slot < nslot ? b.slot_first[slot] : 0u;
+    const uint32_t v = __shfl_sync(FULL, slot_word, slot);
+    const uint32_t f = __shfl_sync(FULL, sfirst, slot);
     const uint32_t smk = v & 0xFFu;
-    const int so = (int)(v >> 8);
-    const uint64_t nw = kNear.w[so];
-    uint32_t nearcr = 0;
-#pragma unroll
-    for (int cr = 0; cr < 8; ++cr) nearcr |= ((uint32_t)(nw >> (8 * cr + c)) & 1u) << cr;
-    const int sx = so % 3 - 1, sy = (so / 3) % 3 - 1, sz = so / 9 - 1;
-    const uint32_t code0 = (uint32_t)(2 * sx + 7 * 2 * sy + 49 * 2 * sz + cc);
-    const bool occ = slot < nslot && ((smk >> c) & 1u);
-    meta[ch] = (occ ? 1u : 0u) | (nearcr << 1) | (code0 << 9);
+    const uint32_t tv = t.cand[(v >> 8) * 8 + c];
+    const bool occ = (smk >> c) & 1u;  // (unused / out-of-grid members: smk = 0)
+    meta[ch] = (occ ? 1u : 0u) | ((tv & 0xFFu) << 1) | ((tv >> 8) << 9);
     rank[ch] = f + __popc(smk & ((1u << c) - 1u));
   }
-  const int64_t w4 = l >= 2 ? __ldg(p.bm[l] + r0) : 0;
-  const int64_t w2 = l == L ? __ldg(p.bm[0] + r0) : 0;
-  const int o4 = (int)(w4 & 3), o4c = (int)(w4 & 15), o2 = (int)(w2 & 3);
-  int k4 = 0, k2 = 0;
+  int64_t* r4 = p.ranks_out[l];
+  int16_t* c4 = p.codes_out[l];
+  int64_t* r2 = p.ranks_out[0];
+  const uint32_t rf = (uint32_t)r0;
   if (l == L) {
-    if (l >= 2) stage_rows<true, true>(own, meta, rank, nch, b, k4, k2, o4, o4c, o2);
-    else stage_rows<false, true>(own, meta, rank, nch, b, k4, k2, o4, o4c, o2);
+    const int64_t w2 = __ldg(p.bm[0] + rf);
+    if (l >= 2) {
+      const int64_t w4 = __ldg(p.bm[l] + rf);
+      write_rows<true, true>(own, meta, rank, r4 + w4, c4 + w4, r2 + w2);
+    } else {
+      write_rows<false, true>(own, meta, rank, nullptr, nullptr, r2 + w2);
+    }
   } else {
-    stage_rows<true, false>(own, meta, rank, nch, b, k4, k2, o4, o4c, o2);
+    const int64_t w4 = __ldg(p.bm[l] + rf);
+    write_rows<true, false>(own, meta, rank, r4 + w4, c4 + w4, nullptr);
   }
-  __syncwarp();
-  if (k4) {
-    flush_ranks(p.ranks_out[l], w4, b.r4, o4, k4, lane);
-    flush_codes(p.codes_out[l], w4, b.c4, o4c, k4, lane);
-  }
-  if (k2) flush_ranks(p.ranks_out[0], w2, b.r2, o2, k2, lane);
-  __syncwarp();  // the slice is refilled by the next parent
 }
 
-__global__ void __launch_bounds__(kSwThreads)
-    k_lists_write_staged(const __grid_constant__ ListsParams p,
-                         const ListsLayout* __restrict__ glay) {
+#ifndef FMMB_LW_MINB
+#define FMMB_LW_MINB 4
+#endif
+__global__ void __launch_bounds__(kLThreads, FMMB_LW_MINB)
+    k_lists_write(const __grid_constant__ ListsParams p, const ListsLayout* __restrict__ glay) {
   __shared__ ListsLayout lay;
-  extern __shared__ __align__(128) unsigned char sw_smem[];
+  __shared__ ListsSmem tab;
   load_layout(glay, lay);
+  load_tables(tab);
   __syncthreads();
   const int L = p.level;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  SwBuf& b = reinterpret_cast<SwBuf*>(sw_smem)[warp];
   const int64_t nwork = lay.work_off[L + 1];
-  const int64_t gstride = (int64_t)gridDim.x * kSwWarps;
-  for (int64_t gw = (int64_t)blockIdx.x * kSwWarps + warp; gw < nwork; gw += gstride) {
+  const int64_t gstride = (int64_t)gridDim.x * kLWarps;
+  for (int64_t gw = (int64_t)blockIdx.x * kLWarps + warp; gw < nwork; gw += gstride) {
     int l = lay.lmin;
     while (lay.work_off[l + 1] <= gw) ++l;
     const int64_t j = gw - lay.work_off[l];
@@ -595,7 +484,7 @@ __global__ void __launch_bounds__(kSwThreads)
       if (lane == 0 && p.ktot[0]) p.ranks_out[0][p.bm[0][0]] = 0;
       continue;
     }
-    write_parent_staged(p, lay, L, l, j, lane, b);
+    write_parent(p, lay, tab, L, l, j, lane);
   }
 }
 
@@ -607,7 +496,6 @@ __global__ void __launch_bounds__(kSwThreads)
 // receiver keys) are scanned in shared memory and offset by a decoupled
 // look-back over the level's tiles (tickets keep tiles in order).  Writes
 // the bookmark arrays and the per-level totals.
-template <bool WRITE>
 __global__ void __launch_bounds__(kLThreads)
     k_lists_cscan(const __grid_constant__ ListsParams p, const ListsLayout* __restrict__ glay,
                   uint64_t* __restrict__ st4, uint64_t* __restrict__ st2,
@@ -737,13 +625,6 @@ __global__ void __launch_bounds__(kLThreads)
     if (l == L) {
       p.bm[0][kr] = base2 + tot2;
       seg_totals[0] = base2 + tot2;
-    }
-  }
-  if (WRITE) {  // fused write: this tile's rows, offsets from the bookmarks just written
-    __syncthreads();
-    for (int k = 0; k < kPW; ++k) {
-      const int64_t j = j0 + warp * kPW + k;
-      if (j < np) write_parent<true>(p, lay, L, l, j, lane);
     }
   }
 }

@@ -320,6 +320,71 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// build_bookmarks / reorder (pseudosort.py:68-78, 105-135) as device passes.
+// k_bm_flags: flags[i] = bins[i] != 0 (np.nonzero), negative bins raise err.
+__global__ void k_bm_flags(const int64_t* __restrict__ bins, int64_t n, int64_t* __restrict__ flags,
+                           uint32_t* __restrict__ err) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = __ldg(bins + i);
+    if (b < 0) atomicOr(err, 1u);
+    flags[i] = b != 0;
+  }
+}
+
+// bookmarks[pos+1] = cumsum(bins[nz]) at nz = i, non_empty[pos] = i
+__global__ void k_bm_write(const int64_t* __restrict__ bins, const int64_t* __restrict__ excl,
+                           const int64_t* __restrict__ pos, int64_t n, int64_t* __restrict__ bm,
+                           uint64_t* __restrict__ ne) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = __ldg(bins + i);
+    if (b != 0) {
+      const int64_t p = __ldg(pos + i);
+      bm[p + 1] = __ldg(excl + i) + b;
+      ne[p] = (uint64_t)i;
+    }
+  }
+}
+
+// permutation[dense_offsets[boxes[i]] + ranks[i]] = i (pseudosort.py:122-125)
+__global__ void k_reorder_perm(const uint64_t* __restrict__ boxes, const int64_t* __restrict__ ranks,
+                               const int64_t* __restrict__ start, int64_t n, int64_t nbins,
+                               int64_t* __restrict__ perm, uint32_t* __restrict__ err) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t b = __ldg(boxes + i);
+    if (b >= (uint64_t)nbins) {
+      atomicOr(err, 1u);
+      continue;
+    }
+    const int64_t p = __ldg(start + b) + __ldg(ranks + i);
+    if (p < 0 || p >= n) {
+      atomicOr(err, 2u);
+      continue;
+    }
+    perm[p] = i;
+  }
+}
+
+// points / charges / boxes gathered through the permutation (pseudosort.py:126-135)
+__global__ void k_reorder_gather(const double* __restrict__ pts, const double* __restrict__ q,
+                                 const uint64_t* __restrict__ boxes,
+                                 const int64_t* __restrict__ perm, int64_t n,
+                                 double* __restrict__ pts_out, double* __restrict__ q_out,
+                                 uint64_t* __restrict__ boxes_out) {
+  for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j < n;
+       j += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t i = __ldg(perm + j);
+    if (i < 0 || i >= n) continue;  // invalid sort index: reported by the host, not read
+    pts_out[3 * j] = __ldg(pts + 3 * i);
+    pts_out[3 * j + 1] = __ldg(pts + 3 * i + 1);
+    pts_out[3 * j + 2] = __ldg(pts + 3 * i + 2);
+    if (q) q_out[j] = __ldg(q + i);
+    boxes_out[j] = __ldg(boxes + i);
+  }
+}
+
 }  // namespace fmmb
 
 // ============================================================ host (C ABI)
@@ -699,4 +764,127 @@ extern "C" fmmb_status fmmb_stencil_segments(fmmb_handle_t h, const uint64_t* re
   if (!bookmark || !alloc || !ranks || !codes || !total) return FMMB_ERR_ARG;
   return segments_impl<true>(h, recv, nr, src, ns, level, bookmark, alloc, ctx, ranks, codes,
                              total, (cudaStream_t)stream);
+}
+
+
+namespace {
+
+// bookmarks + non-empty indices of a dense histogram (shared by
+// fmmb_build_bookmarks and fmmb_reorder); `excl` = exclusive scan of bins
+fmmb_status bookmarks_impl(fmmb_handle_t h, Workspace& ws, const int64_t* bins, int64_t nbins,
+                           const int64_t* excl, fmmb_alloc_fn alloc, void* ctx,
+                           int64_t** bookmarks, uint64_t** non_empty, int64_t* k) {
+  cudaStream_t s = ws.s;
+  int64_t* flags = ws.take<int64_t>(nbins);
+  int64_t* pos = ws.take<int64_t>(nbins);
+  uint32_t* err = ws.take<uint32_t>(1);
+  if (ws.overflow) return fmmb_fail(h, FMMB_ERR_CUDA, "internal: workspace overflow");
+  cudaMemsetAsync(err, 0, 4, s);
+  k_bm_flags<<<grid_for(nbins, 256, h->num_sms), 256, 0, s>>>(bins, nbins, flags, err);
+  ++h->launches;
+  ScanResult sr;
+  if (!scan_i64(h, ws, flags, nbins, pos, false, &sr, &h->launches))
+    return cuda_status(h, "build_bookmarks scan");
+  const int64_t K = sr.total;
+  int64_t* bm = (int64_t*)alloc(ctx, (uint64_t)(K + 1) * 8);
+  uint64_t* ne = (uint64_t*)alloc(ctx, (uint64_t)std::max<int64_t>(K, 1) * 8);
+  if (!bm || !ne) return fmmb_fail(h, FMMB_ERR_ALLOC, "bookmark allocation failed");
+  cudaMemsetAsync(bm, 0, 8, s);
+  k_bm_write<<<grid_for(nbins, 256, h->num_sms), 256, 0, s>>>(bins, excl, pos, nbins, bm, ne);
+  ++h->launches;
+  *bookmarks = bm;
+  *non_empty = ne;
+  *k = K;
+  return cuda_status(h, "build_bookmarks");
+}
+
+}  // namespace
+
+extern "C" fmmb_status fmmb_build_bookmarks(fmmb_handle_t h, const int64_t* bins, int64_t nbins,
+                                            fmmb_alloc_fn alloc, void* ctx, int64_t** bookmarks,
+                                            uint64_t** non_empty, int64_t* k, void* stream) {
+  FMMB_GUARD(h);
+  FMMB_ENTER(h);
+  if (!alloc || !bookmarks || !non_empty || !k || nbins < 0 || (nbins > 0 && !bins))
+    return FMMB_ERR_ARG;
+  cudaStream_t s = (cudaStream_t)stream;
+  *bookmarks = nullptr;
+  *non_empty = nullptr;
+  *k = 0;
+  if (nbins == 0) {
+    int64_t* bm = (int64_t*)alloc(ctx, 8);
+    uint64_t* ne = (uint64_t*)alloc(ctx, 8);
+    if (!bm || !ne) return fmmb_fail(h, FMMB_ERR_ALLOC, "bookmark allocation failed");
+    cudaMemsetAsync(bm, 0, 8, s);
+    *bookmarks = bm;
+    *non_empty = ne;
+    return cuda_status(h, "build_bookmarks");
+  }
+  Workspace ws(s);
+  if (!ws.reserve(3 * slice(nbins, 8) + 2 * slice(ceil_div(nbins, kXTile) + 1, 8) + 16384))
+    return fmmb_fail(h, FMMB_ERR_CUDA, "workspace allocation failed");
+  int64_t* excl = ws.take<int64_t>(nbins);
+  ScanResult sr;
+  if (!scan_i64(h, ws, bins, nbins, excl, false, &sr, &h->launches))
+    return cuda_status(h, "build_bookmarks scan");
+  if (sr.err & 2u) return fmmb_fail(h, FMMB_ERR_DOMAIN, "histogram counts must be non-negative");
+  return bookmarks_impl(h, ws, bins, nbins, excl, alloc, ctx, bookmarks, non_empty, k);
+}
+
+extern "C" fmmb_status fmmb_reorder(fmmb_handle_t h, const double* points, const double* charges,
+                                    int64_t n, const int64_t* bins, int64_t nbins,
+                                    const uint64_t* boxes, const int64_t* ranks, int level,
+                                    fmmb_alloc_fn alloc, void* ctx, fmmb_point_set* out,
+                                    void* stream) {
+  FMMB_GUARD(h);
+  FMMB_ENTER(h);
+  if (!alloc || !out || n < 0 || nbins < 1 || !bins || (n > 0 && (!points || !boxes || !ranks)))
+    return FMMB_ERR_ARG;
+  (void)level;
+  cudaStream_t s = (cudaStream_t)stream;
+  memset(out, 0, sizeof(*out));
+  Workspace ws(s);
+  if (!ws.reserve(3 * slice(nbins, 8) + 2 * slice(ceil_div(nbins, kXTile) + 1, 8) + 16384))
+    return fmmb_fail(h, FMMB_ERR_CUDA, "workspace allocation failed");
+  int64_t* excl = ws.take<int64_t>(nbins);
+  uint32_t* err = ws.take<uint32_t>(1);
+  cudaMemsetAsync(err, 0, 4, s);
+  ScanResult sr;
+  if (!scan_i64(h, ws, bins, nbins, excl, false, &sr, &h->launches))
+    return cuda_status(h, "reorder scan");
+  if (sr.err & 2u) return fmmb_fail(h, FMMB_ERR_DOMAIN, "histogram counts must be non-negative");
+  const size_t nn = (size_t)std::max<int64_t>(n, 1);
+  double* pts_out = (double*)alloc(ctx, nn * 24);
+  double* q_out = charges ? (double*)alloc(ctx, nn * 8) : nullptr;
+  int64_t* perm = (int64_t*)alloc(ctx, nn * 8);
+  uint64_t* bx_out = (uint64_t*)alloc(ctx, nn * 8);
+  if (!pts_out || (charges && !q_out) || !perm || !bx_out)
+    return fmmb_fail(h, FMMB_ERR_ALLOC, "reorder output allocation failed");
+  if (n > 0) {
+    cudaMemsetAsync(perm, 0xFF, (size_t)n * 8, s);  // unset positions stay -1 (never gathered)
+    k_reorder_perm<<<grid_for(n, 256, h->num_sms), 256, 0, s>>>(boxes, ranks, excl, n, nbins,
+                                                                  perm, err);
+    k_reorder_gather<<<grid_for(n, 256, h->num_sms), 256, 0, s>>>(points, charges, boxes, perm,
+                                                                    n, pts_out, q_out, bx_out);
+    h->launches += 2;
+  }
+  cudaMemcpyAsync(h->pinned, err, 4, cudaMemcpyDeviceToHost, s);
+  if (cudaStreamSynchronize(s) != cudaSuccess) return cuda_status(h, "reorder");
+  const uint32_t herr = *(uint32_t*)h->pinned;
+  if (herr & 1u) return fmmb_fail(h, FMMB_ERR_DOMAIN, "box index outside [0, nbins)");
+  if (herr & 2u) return fmmb_fail(h, FMMB_ERR_DOMAIN, "sort index position outside [0, n)");
+  int64_t* bm = nullptr;
+  uint64_t* ne = nullptr;
+  int64_t K = 0;
+  const fmmb_status st = bookmarks_impl(h, ws, bins, nbins, excl, alloc, ctx, &bm, &ne, &K);
+  if (st != FMMB_OK) return st;
+  out->points = pts_out;
+  out->charges = q_out;
+  out->permutation = perm;
+  out->bookmarks = bm;
+  out->non_empty = ne;
+  out->boxes = bx_out;
+  out->n = n;
+  out->k = K;
+  return cuda_status(h, "reorder");
 }

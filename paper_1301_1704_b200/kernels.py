@@ -221,24 +221,31 @@ def exclusive_scan(values):
 
 def build_bookmarks(bins):
     """(bookmarks, non-empty box indices) from a dense histogram
-    (pseudosort.py:68-78)."""
+    (pseudosort.py:68-78): fmmb_build_bookmarks (flag scan + compaction on
+    the device)."""
     dev = _host.pick_device(bins)
     dout = _host.is_device_input(bins)
     b = _host.to_device(bins, dev, torch.int64, (-1,))
-    if b.numel() == 0:
-        z = torch.zeros(1, dtype=torch.int64, device=dev)
-        return _out(z, dout), _out(torch.empty(0, dtype=torch.uint64, device=dev), dout)
-    starts, total = exclusive_scan(b)
-    nz = torch.nonzero(b > 0).reshape(-1)
-    bm = torch.empty(nz.numel() + 1, dtype=torch.int64, device=dev)
-    bm[0] = 0
-    bm[1:] = starts[nz] + b[nz]
-    return _out(bm, dout), _out(nz.to(torch.int64).view(torch.uint64), dout)
+    lib = _lib.load()
+    h = _lib.handle(dev)
+    alloc = _lib.Allocator(dev)
+    bm_p, ne_p, k = C.c_void_p(), C.c_void_p(), C.c_int64(0)
+    st = lib.fmmb_build_bookmarks(h, _ptr(b), b.numel(), alloc.fn, None, C.byref(bm_p),
+                                  C.byref(ne_p), C.byref(k), _lib.stream_of(dev))
+    if alloc.error is not None:
+        raise alloc.error
+    _lib.check(st, h)
+    kk = int(k.value)
+    bm = _lib.view(alloc, bm_p.value, kk + 1, "i8")
+    ne = _lib.view(alloc, ne_p.value, kk, "u8")
+    return _out(bm, dout), _out(ne, dout)
 
 
 def reorder(points, charges, bins, boxes, ranks, max_level: int):
-    """Box-grouped copy from a (bins, boxes, ranks) sort index (pseudosort.py:105-135)."""
-    from .pseudosort import SortedPointSet
+    """Box-grouped copy from a (bins, boxes, ranks) sort index
+    (pseudosort.py:105-135): fmmb_reorder (permutation scatter, gather of
+    points / charges / boxes, bookmarks) on the device."""
+    from .pseudosort import _point_set_from_c
 
     dev = _host.pick_device(points, charges, bins, boxes, ranks)
     dout = _host.is_device_input(points, charges, bins, boxes, ranks)
@@ -249,18 +256,26 @@ def reorder(points, charges, bins, boxes, ranks, max_level: int):
     if bx.numel() != n or rk.numel() != n:
         raise DomainError("points and sort index lengths disagree")
     bn = _host.to_device(bins, dev, torch.int64, (-1,))
-    starts, _ = exclusive_scan(bn)
-    positions = starts[bx.view(torch.int64)] + rk
-    perm = torch.empty(n, dtype=torch.int64, device=dev)
-    perm[positions] = torch.arange(n, dtype=torch.int64, device=dev)
-    bm, nz = build_bookmarks(bn)
+    if bn.numel() == 0:
+        if n:
+            raise DomainError("box index outside [0, nbins)")
+        bn = torch.zeros(1, dtype=torch.int64, device=dev)  # same (empty) outputs
     q = None
     if charges is not None:
-        q = _host.to_device(charges, dev, torch.float64, (-1,))[perm]
-    res = SortedPointSet(level=max_level, points=pts[perm], charges=q, permutation=perm,
-                         bookmarks=bm if isinstance(bm, torch.Tensor) else torch.from_numpy(bm),
-                         non_empty_index=nz if isinstance(nz, torch.Tensor) else torch.from_numpy(nz),
-                         boxes=bx.view(torch.int64)[perm].view(torch.uint64))
+        q = _host.to_device(charges, dev, torch.float64, (-1,))
+        if q.numel() < n:
+            raise DomainError("charges shorter than points")
+    lib = _lib.load()
+    h = _lib.handle(dev)
+    alloc = _lib.Allocator(dev)
+    out = _lib.PointSetC()
+    st = lib.fmmb_reorder(h, _ptr(pts), _ptr(q) if q is not None else None, n, _ptr(bn),
+                          bn.numel(), _ptr(bx), _ptr(rk), int(max_level), alloc.fn, None,
+                          C.byref(out), _lib.stream_of(dev))
+    if alloc.error is not None:
+        raise alloc.error
+    _lib.check(st, h)
+    res = _point_set_from_c(out, alloc, max_level, q is not None)
     return res if dout else res.to_numpy()
 
 

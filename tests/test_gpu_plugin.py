@@ -124,3 +124,47 @@ def test_install_into_reference(ref, K):
     from tests.parity import compare_structures
 
     assert not compare_structures(st, want)
+
+
+def test_build_bookmarks_and_reorder_match_oracle(K):
+    """kernels.build_bookmarks / kernels.reorder (pseudosort.py:68-78, 105-135)
+    on the device vs the C restatement, numpy and CUDA in/out."""
+    src, q, _ = generate(40000, 1, "sphere", 11)
+    for L in (1, 3, 5):
+        boxes = orc.encode(src, L)
+        bins, ranks = K.assign_box_ranks(boxes, 8**L)
+        bm, ne = K.build_bookmarks(bins)
+        obm, one = orc.build_bookmarks(bins)
+        assert bm.dtype == np.int64 and ne.dtype == np.uint64
+        assert np.array_equal(bm, obm) and np.array_equal(ne, one)
+        got = K.reorder(src, q, bins, boxes, ranks, L)
+        want = orc.reorder(src, q, bins, boxes, ranks)
+        for f in ("points", "charges", "permutation", "bookmarks", "non_empty_index", "boxes"):
+            a, b = np.asarray(getattr(got, f)), getattr(want, f)
+            assert a.dtype == b.dtype and np.array_equal(a, b), (L, f)
+        nq = K.reorder(src, None, bins, boxes, ranks, L)
+        assert nq.charges is None and np.array_equal(nq.points, want.points)
+    # device in -> device out
+    dev = torch.device("cuda", 0)
+    bins_d = torch.tensor([0, 3, 0, 0, 2, 1], dtype=torch.int64, device=dev)
+    bm, ne = K.build_bookmarks(bins_d)
+    assert bm.is_cuda and bm.cpu().tolist() == [0, 3, 5, 6]
+    assert ne.view(torch.int64).cpu().tolist() == [1, 4, 5]
+    # empty and all-zero histograms
+    bm, ne = K.build_bookmarks(np.zeros(0, np.int64))
+    assert bm.tolist() == [0] and ne.size == 0
+    bm, ne = K.build_bookmarks(np.zeros(9, np.int64))
+    assert bm.tolist() == [0] and ne.size == 0
+
+
+def test_reorder_rejects_bad_sort_index(K):
+    from paper_1301_1704_b200.errors import DomainError
+
+    pts = np.random.default_rng(0).random((10, 3))
+    boxes = np.zeros(10, np.uint64)
+    with pytest.raises(DomainError):
+        K.reorder(pts, None, np.array([10], np.int64), boxes[:5], np.arange(5), 0)
+    with pytest.raises(DomainError):  # box index outside the histogram
+        K.reorder(pts, None, np.array([10], np.int64), boxes + 3, np.arange(10), 0)
+    with pytest.raises(DomainError):
+        K.build_bookmarks(np.array([1, -2, 3], np.int64))

@@ -120,3 +120,65 @@ def test_algorithmic_bytes_c2_from_survey_counts():
     c["s_l"] = s_l
     assert sum(s_l.values()) == 435_312_397
     assert roofline.build_bytes(c) == 7_322_505_058
+
+
+def _morton(x, y, z):
+    k = 0
+    for b in range(21):
+        k |= ((x >> b) & 1) << (3 * b) | ((y >> b) & 1) << (3 * b + 1) | ((z >> b) & 1) << (3 * b + 2)
+    return k
+
+
+def _window_order_table():
+    """Host restatement of lists.cuh WinOrder: 48 cases (3 parities x the
+    ranking of K_a * 3 + a), each the 27 window offsets in Morton order."""
+    ranks = [(0, 1, 2), (0, 2, 1), (1, 0, 2), (1, 2, 0), (2, 0, 1), (2, 1, 0)]
+    tab = []
+    for cs in range(48):
+        c = []
+        for a in range(3):
+            K = ranks[cs >> 3][a] + 1
+            c.append((3 << K) - 1 if (cs >> a) & 1 else 3 << K)
+        keys = [_morton(c[0] + q % 3 - 1, c[1] + (q // 3) % 3 - 1, c[2] + q // 9 - 1)
+                for q in range(27)]
+        tab.append(sorted(range(27), key=lambda q: keys[q]))
+    return tab
+
+
+def _window_case(x, y, z, l1):
+    par, kk = 0, []
+    for a, v in enumerate((x, y, z)):
+        odd = v & 1
+        w = v + 1 if odd else v
+        K = ((w & -w).bit_length() - 1) if (w and w < (1 << l1)) else 64
+        par |= odd << a
+        kk.append(K * 3 + a)
+    rx = (kk[0] > kk[1]) + (kk[0] > kk[2])
+    ry = (kk[1] > kk[0]) + (kk[1] > kk[2])
+    pi = (0 if ry == 1 else 1) if rx == 0 else (2 if ry == 0 else 3) if rx == 1 else (
+        4 if ry == 0 else 5)
+    return par | (pi << 3)
+
+
+def test_window_order_table_matches_sorted_windows():
+    """The list writer's table-driven window order (lists.cuh window_case /
+    WinOrder) equals sorting the in-grid 3x3x3 window keys, at every level
+    and at the grid faces."""
+    import random
+
+    tab = _window_order_table()
+    rng = random.Random(7)
+    for l1 in range(0, 9):
+        n = 1 << l1
+        pts = {(0, 0, 0), (n - 1, n - 1, n - 1), (0, n - 1, 0)}
+        pts |= {tuple(rng.randrange(n) for _ in range(3)) for _ in range(300)}
+        for x, y, z in pts:
+            members = []
+            for q in range(27):
+                p = (x + q % 3 - 1, y + (q // 3) % 3 - 1, z + q // 9 - 1)
+                if all(0 <= v < n for v in p):
+                    members.append((_morton(*p), q))
+            want = [q for _, q in sorted(members)]
+            inside = {q for _, q in members}
+            got = [q for q in tab[_window_case(x, y, z, l1)] if q in inside]
+            assert got == want, (l1, x, y, z)
