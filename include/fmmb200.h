@@ -170,6 +170,12 @@ FMMB_API fmmb_status fmmb_build_bookmarks(fmmb_handle_t h, const int64_t* bins,
                                  int64_t** bookmarks, uint64_t** non_empty,
                                  int64_t* k, void* stream);
 
+/* Workload driver (c4 dynamic rebuild; not a reference entry point):
+ * x[i] <- mod(x[i] + N(0, scale^2), 1.0) in place, np.mod's convention,
+ * normals from Philox4x32-10 keyed by (seed, step). */
+FMMB_API fmmb_status fmmb_perturb(fmmb_handle_t h, double* x, int64_t n, uint64_t seed,
+                         uint64_t step, double scale, void* stream);
+
 /* --------------------------------------------------------- build API level */
 
 /* One sorted point set, reference layout (pseudosort.py:81-102). */

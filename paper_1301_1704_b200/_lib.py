@@ -78,6 +78,7 @@ SIGNATURES = [
      [_p, _p, _i64, ALLOC_FN, _p, C.POINTER(_p), C.POINTER(_p), C.POINTER(_i64), _p]),
     ("fmmb_reorder", C.c_int,
      [_p, _p, _p, _i64, _p, _i64, _p, _p, C.c_int, ALLOC_FN, _p, C.POINTER(PointSetC), _p]),
+    ("fmmb_perturb", C.c_int, [_p, _p, _i64, C.c_uint64, C.c_uint64, C.c_double, _p]),
     ("fmmb_build_all", C.c_int,
      [_p, _p, _p, _i64, _p, _i64, C.c_int, ALLOC_FN, _p, C.POINTER(StructuresC), _p, _p]),
     ("fmmb_sort_points", C.c_int,
@@ -244,7 +245,27 @@ class Allocator:
                 return b, ptr - base
         raise NativeError(f"pointer {ptr:#x} is not in any allocated block")
 
+    def typed(self, ptr: int, tdt: torch.dtype, size: int) -> tuple[torch.Tensor, int] | None:
+        """(whole block viewed as `tdt`, element offset of ptr), cached per
+        block and dtype, when the block and the offset are `size`-aligned:
+        one slicing op per output view instead of three."""
+        cache = self.__dict__.setdefault("_typed", {})
+        for i, b in enumerate(self.blocks):
+            base = b.data_ptr()
+            n = b.numel()
+            if base <= ptr < base + n or ptr == base:
+                off = ptr - base
+                if off % size or n % size:
+                    return None
+                t = cache.get((i, tdt))
+                if t is None:
+                    t = b.view(tdt)
+                    cache[(i, tdt)] = t
+                return t, off // size
+        raise NativeError(f"pointer {ptr:#x} is not in any allocated block")
 
+
+_SIZES = {"f8": 8, "i8": 8, "u8": 8, "i2": 2, "u4": 4, "i4": 4}
 _TORCH_DTYPES = {
     "f8": torch.float64, "i8": torch.int64, "u8": torch.uint64, "i2": torch.int16,
     "u4": torch.uint32, "i4": torch.int32,
@@ -257,10 +278,13 @@ def view(alloc: Allocator, ptr: int | None, count: int, dtype: str, shape=None) 
     if not ptr or count == 0:
         t = torch.empty(0, dtype=tdt, device=alloc.dev)
         return t.reshape(shape if shape is not None else (0,)) if shape is not None else t
-    block, off = alloc.block_of(ptr)
-    size = torch.empty(0, dtype=tdt).element_size()
-    raw = block[off: off + count * size]
-    t = raw.view(tdt)
+    size = _SIZES[dtype]
+    tv = alloc.typed(ptr, tdt, size)
+    if tv is not None:
+        t = tv[0][tv[1]: tv[1] + count]
+    else:
+        block, off = alloc.block_of(ptr)
+        t = block[off: off + count * size].view(tdt)
     if shape is not None:
         t = t.view(*shape)
     return t
@@ -275,3 +299,42 @@ def trace(dev) -> list[tuple[str, float]]:
     names = (C.c_char_p * 32)()
     k = lib.fmmb_trace(h, ms, names, 32)
     return [(names[i].decode(), float(ms[i])) for i in range(k)]
+
+
+class EventRing:
+    """Per-device ring of 6-event sets for the build's phase timing: events
+    are created once and reused; a slot's previous owner (a lazily resolved
+    BuildSeconds) is resolved before its events are recorded again."""
+
+    SIZE = 64
+
+    def __init__(self):
+        self.sets: list = []
+        self.owners: list = [None] * self.SIZE
+        self.i = 0
+
+    def take(self, owner):
+        import weakref
+
+        k = self.i % self.SIZE
+        self.i += 1
+        if k == len(self.sets):
+            evs = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
+            for e in evs:  # torch creates the CUevent lazily, on first record
+                e.record()
+            self.sets.append((evs, (C.c_void_p * 6)(*[e.cuda_event for e in evs])))
+        prev = self.owners[k]() if self.owners[k] is not None else None
+        if prev is not None:
+            prev._resolve()
+        self.owners[k] = weakref.ref(owner)
+        return self.sets[k]
+
+
+_rings: dict[int, EventRing] = {}
+
+
+def event_ring(dev: torch.device) -> EventRing:
+    r = _rings.get(dev.index)
+    if r is None:
+        r = _rings[dev.index] = EventRing()
+    return r

@@ -271,8 +271,12 @@ void launch_local(fmmb_handle_t h, const double* rec, uint32_t* idx, const uint3
                   const BucketGeo& g, int L, const LocalOut& o, uint64_t* lst,
                   const uint32_t* fail, cudaStream_t s) {
   auto kern = k_bkt_local<CK, NARROW, HEADS>;
-  int per_sm = 1;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kLcThreads, lc_smem_bytes<CK>());
+  static const int occ = [&] {  // resident CTAs per SM (same on every B200), once
+    int v = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, kern, kLcThreads, lc_smem_bytes<CK>());
+    return v;
+  }();
+  int per_sm = occ;
   if (h->lc_per_sm > 0) per_sm = std::min(per_sm, h->lc_per_sm);
   const int grid = std::max(1, per_sm) * h->num_sms;  // persistent: all CTAs resident
   kern<<<grid, kLcThreads, lc_smem_bytes<CK>(), s>>>(rec, idx, bstart_f, rbase, desc, nfinal, g,
@@ -1018,3 +1022,4 @@ extern "C" fmmb_status fmmb_sort_points(fmmb_handle_t h, const double* points,
 #include "nearfield.cuh"
 #include "boxtype.cuh"
 #include "partplan.cuh"
+#include "workload.cuh"

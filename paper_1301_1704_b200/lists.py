@@ -222,13 +222,12 @@ def build_all_device(src: torch.Tensor, charges: torch.Tensor | None, recv: torc
         raise DomainError("charges and source points lengths disagree")
     alloc = _lib.Allocator(dev)
     out = _lib.StructuresC()
-    events = None
+    secs = None
     ev_arr = None
-    if timing:
-        events = [torch.cuda.Event(enable_timing=True) for _ in range(6)]
-        for e in events:  # torch creates the CUevent lazily, on first record
-            e.record()
-        ev_arr = (C.c_void_p * 6)(*[e.cuda_event for e in events])
+    if timing:  # reused event sets (EventRing), resolved lazily
+        secs = BuildSeconds(None)
+        events, ev_arr = _lib.event_ring(dev).take(secs)
+        secs._events = events
     st = lib.fmmb_build_all(
         h, src.data_ptr() if n else None,
         charges.data_ptr() if (charges is not None and n) else None, n,
@@ -237,7 +236,9 @@ def build_all_device(src: torch.Tensor, charges: torch.Tensor | None, recv: torc
     if alloc.error is not None:
         raise alloc.error
     _lib.check(st, h)
-    res = _structures_from_c(out, alloc, charges is not None, events)
+    res = _structures_from_c(out, alloc, charges is not None, None)
+    if secs is not None:
+        res.build_seconds = secs
     res.sort_path = _lib.SORT_PATHS.get(int(lib.fmmb_last_sort_path(h)), "")
     return res
 

@@ -86,15 +86,18 @@ def c4_step_inputs(n: int = 2**23, seed: int = 4, steps: int = 1):
     return src, q, recv
 
 
-def perturb_device(points, gen, scale: float = 1e-3):
-    """c4 rebuild step on the device, in place: x <- remainder(x + N(0, scale), 1.0)
-    (torch's float remainder is fmod plus the sign fix-up, the same
-    operations as np.mod, so a tiny negative sum maps to exactly 1.0 too).
-    `gen` is a CUDA torch.Generator; the trajectory is reproducible from its
-    seed.  Workload driver only (not part of the build path)."""
-    import torch
+def perturb_device(points, seed: int, step: int, scale: float = 1e-3):
+    """c4 rebuild step on the device, in place: x <- mod(x + N(0, scale), 1.0)
+    in one fused libfmmb200 pass (fmmb_perturb: Philox4x32-10 normals keyed
+    by (seed, step), np.mod's convention, so a tiny negative sum maps to
+    exactly 1.0).  Workload driver only (not part of the build path)."""
+    from . import _lib
 
-    noise = torch.randn(points.shape, generator=gen, device=points.device, dtype=points.dtype)
-    points.add_(noise.mul_(scale))
-    torch.remainder(points, 1.0, out=points)
+    if not (points.is_cuda and points.dtype.is_floating_point and points.is_contiguous()):
+        raise FmmError("perturb_device needs a contiguous f64 CUDA tensor")
+    dev = _lib.device_of(points.device)
+    h = _lib.handle(dev)
+    st = _lib.load().fmmb_perturb(h, points.data_ptr(), points.numel(), int(seed) & (2**64 - 1),
+                                  int(step), float(scale), _lib.stream_of(dev))
+    _lib.check(st, h)
     return points

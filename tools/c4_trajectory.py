@@ -51,8 +51,6 @@ def main():
     src = torch.from_numpy(src_np).to(dev)
     q = torch.from_numpy(q_np).to(dev)
     recv = torch.from_numpy(recv_np).to(dev)
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(a.seed)
     stream = torch.cuda.current_stream(dev)
     n_part = 2 * wl.n
     # warm-up rebuilds on the unperturbed state (allocator, handle)
@@ -65,8 +63,8 @@ def main():
     for k in range(a.steps):
         e0, e1, e2 = (torch.cuda.Event(enable_timing=True) for _ in range(3))
         e0.record(stream)
-        perturb_device(src, gen)
-        perturb_device(recv, gen)
+        perturb_device(src, a.seed, 2 * k + 2)
+        perturb_device(recv, a.seed, 2 * k + 3)
         e1.record(stream)
         st = fb.build_all_device(src, q, recv, wl.level, timing=False)
         e2.record(stream)
