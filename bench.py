@@ -39,6 +39,7 @@ ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
 METRIC = "particles/sec for full FMM data-structure build"
+NVLINK_GBS = 900.0  # NVLink 5 per direction per B200 (nominal)
 UNIT = "particles/s"
 
 
@@ -473,9 +474,10 @@ def run_partitioned(args):
     n_glob = n_per * ws
     comm = D.TorchComm()
     ops = D.DeviceOps()
+    timer = [None]
 
     def step():
-        return D.build_all_distributed([(src, q, recv)], L, comm, ops=ops)[0]
+        return D.build_all_distributed([(src, q, recv)], L, comm, ops=ops, timer=timer[0])[0]
 
     sh = None
     for _ in range(max(args.warmup, 3)):
@@ -483,6 +485,7 @@ def run_partitioned(args):
         sh = step()
     pts = int(sh.sorted_src.points.shape[0] + sh.sorted_recv.points.shape[0])
     sent = int(sh.exchanged["sent_points"])
+    sent_bytes = int(sh.exchanged.get("sent_bytes", 0))
     lists_bytes = 8 * int(sh.neighbor_table.neighbor_list.shape[0]) + sum(
         10 * int(v.shape[0]) for v in sh.stencils.ranks.values())
     sh = None
@@ -495,6 +498,7 @@ def run_partitioned(args):
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ops.launches = 0
+    timer[0] = D.PhaseTimer()
     ev0.record(stream)
     for _ in range(args.steps):
         sh = step()
@@ -507,9 +511,19 @@ def run_partitioned(args):
     t = torch.tensor([ev0.elapsed_time(ev1) * 1e-3], device=dev, dtype=torch.float64)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     elapsed = float(t.item())
-    agg = torch.tensor([pts, sent, lists_bytes], device=dev, dtype=torch.int64)
+    agg = torch.tensor([pts, sent, lists_bytes, sent_bytes], device=dev, dtype=torch.int64)
     dist.all_reduce(agg)
-    pts_all, sent_all, lists_all = (int(x) for x in agg.tolist())
+    pts_all, sent_all, lists_all, sent_bytes_all = (int(x) for x in agg.tolist())
+    # per-phase device time (events on this rank's stream), max over ranks
+    ph = timer[0].ms()
+    names = sorted(ph)
+    pt = torch.tensor([ph[k] / args.steps for k in names], device=dev, dtype=torch.float64)
+    dist.all_reduce(pt, op=dist.ReduceOp.MAX)
+    phases = {k: float(v) for k, v in zip(names, pt.tolist())}
+    ex_ms = sum(v for k, v in phases.items() if k.startswith("exchange"))
+    sent_max = torch.tensor([sent_bytes], device=dev, dtype=torch.int64)
+    dist.all_reduce(sent_max, op=dist.ReduceOp.MAX)
+    sent_max = int(sent_max.item())
     ms_step = elapsed / args.steps * 1e3
     value = 2 * n_glob * args.steps / elapsed
     # per-GPU algorithmic bytes: inputs + sorted outputs (SURVEY 8(d), 80/64 B per
@@ -518,10 +532,34 @@ def run_partitioned(args):
     achieved = per_gpu_bytes / (elapsed / args.steps) / 1e9
     peak, peak_src = roofline.measured_hbm_gbs(ROOT)
     e2e = None
+    e2e_note = None
     if not args.no_e2e:
-        h_src = src.cpu().pin_memory()
-        h_q = q.cpu().pin_memory()
-        h_recv = recv.cpu().pin_memory()
+        e_src, e_q, e_recv, e_L, e_n = src, q, recv, L, n_glob
+        # host outputs of one rank ~ 200 B per particle; with every local
+        # rank holding them, stay within ~1/3 of the host's available RAM
+        # (a c5 shard is ~60 GB of numpy outputs per rank): else measure the
+        # end-to-end path on c2-size shards (2^24 + 2^24 per rank)
+        try:
+            avail = os.sysconf("SC_AVPHYS_PAGES") * os.sysconf("SC_PAGE_SIZE")
+        except (ValueError, OSError):
+            avail = 0
+        local_ranks = int(os.environ.get("LOCAL_WORLD_SIZE", str(ws)))
+        need = 200 * 2 * n_per * local_ranks * 2
+        if avail and need > avail / 3 and n_per > 2**24:
+            g2 = torch.Generator(device=dev)
+            g2.manual_seed(7 + rank)
+            e_n = 2**24
+            e_src = torch.rand((e_n, 3), generator=g2, device=dev, dtype=torch.float64)
+            e_recv = torch.rand((e_n, 3), generator=g2, device=dev, dtype=torch.float64)
+            e_q = torch.randn(e_n, generator=g2, device=dev, dtype=torch.float64)
+            e_L = choose_max_level(e_n * ws, 16)
+            e_n = e_n * ws
+            e2e_note = (f"c2-size shards (N=M=2^24 per rank, max_level={e_L}): the {wl.name} "
+                        f"host outputs ({need / 1e9:.0f} GB on this node) exceed 1/3 of the "
+                        f"available host RAM ({avail / 1e9:.0f} GB)")
+        h_src = e_src.cpu().pin_memory()
+        h_q = e_q.cpu().pin_memory()
+        h_recv = e_recv.cpu().pin_memory()
         times = []
         d2h = 0
         for _ in range(max(1, args.e2e_steps)):
@@ -530,16 +568,28 @@ def run_partitioned(args):
             t0 = time.perf_counter()
             shard = [(h_src.to(dev, non_blocking=True), h_q.to(dev, non_blocking=True),
                       h_recv.to(dev, non_blocking=True))]
-            out = D.build_all_distributed(shard, L, comm)[0].to_numpy()
+            out = D.build_all_distributed(shard, e_L, comm)[0].to_numpy()
             dt = torch.tensor([time.perf_counter() - t0], device=dev, dtype=torch.float64)
             dist.all_reduce(dt, op=dist.ReduceOp.MAX)
             times.append(float(dt.item()))
             d2h = _numpy_bytes_shard(out)
             out = None
         h2d = (h_src.numel() + h_q.numel() + h_recv.numel()) * 8
-        e2e = {"value": 2 * n_glob / statistics.median(times), "unit": UNIT,
+        e2e = {"value": 2 * e_n / statistics.median(times), "unit": UNIT,
                "h2d_bytes_per_step": int(h2d * ws), "d2h_bytes_per_step": int(d2h * ws),
                "ms_per_step": statistics.median(times) * 1e3}
+        if e2e_note:
+            e2e["workload"] = e2e_note
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        # the reference CPU build of c2 on identical arrays (rank 0 only, after
+        # the timed region); the c5 problem (2^31 points) does not fit the
+        # host, so its CPU rate is extrapolated at c2's per-particle rate
+        rate, kind, cores, sample, _, _ = cpu_reference_rate("c2", steps=1)
+        cpu = {"value": rate, "unit": UNIT, "cores": cores, "kind": kind,
+               "sample": sample + "; extrapolated to this workload at the same "
+                                  "per-particle rate (the global problem exceeds host memory)"}
+    dist.barrier()
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
@@ -559,12 +609,20 @@ def run_partitioned(args):
                 "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "peak_source": peak_src, "traffic": None,
             },
-            "exchange": {"points_sent": sent_all,
-                         "bytes_sent": sent_all * 40,
-                         "nvlink_gbs_per_gpu_at_step": sent_all * 40 / ws / (elapsed / args.steps) / 1e9},
+            "exchange": {
+                "points_sent": sent_all, "bytes_sent": sent_bytes_all,
+                "max_bytes_sent_per_gpu": sent_max, "ms": ex_ms,
+                "nvlink_roofline": {
+                    "bound": "nvlink", "unit": "GB/s",
+                    "achieved": (sent_max / (ex_ms * 1e-3) / 1e9) if ex_ms > 0 else None,
+                    "peak": NVLINK_GBS, "peak_source": "nominal NVLink 5, per direction per GPU",
+                    "frac": (sent_max / (ex_ms * 1e-3) / 1e9 / NVLINK_GBS) if ex_ms > 0 else None},
+            },
+            "phases_ms": phases,
+            "max_memory_gb_rank0": torch.cuda.max_memory_allocated(dev) / 1e9,
             "clocks": clk,
             "e2e": e2e,
-            "cpu_baseline": None,
+            "cpu_baseline": cpu,
             "gpu_launches": int(launches),
         }
         print(json.dumps(line), flush=True)

@@ -47,7 +47,7 @@ from .lists import FmmStructures, LevelDirectory, NeighborTable, TranslationSten
 from .pseudosort import SortedPointSet, _point_set_from_c, check_level
 
 __all__ = [
-    "Comm", "TorchComm", "SimComm", "DeviceOps", "DistShard", "build_all_distributed",
+    "Comm", "TorchComm", "SimComm", "DeviceOps", "DistShard", "PhaseTimer", "build_all_distributed",
     "cut_bins", "concat_shards", "partition_bits",
 ]
 
@@ -394,9 +394,32 @@ class DistShard:
     exchanged: dict = field(default_factory=dict)  # points sent to other ranks
 
     def to_numpy(self) -> "DistShard":
-        """Host copy of the shard (numpy arrays, reference dtypes)."""
+        """Host copy of the shard (numpy arrays, reference dtypes): every
+        array copied into pinned host memory on the build stream, one sync."""
+        from ._host import HostBatch
+
+        batch = HostBatch()
+        staged = {}
+
         def npy(v):
-            return v.cpu().numpy() if isinstance(v, torch.Tensor) else v
+            if not isinstance(v, torch.Tensor):
+                return v
+            if not v.is_cuda:
+                return v.numpy()
+            key = (v.data_ptr(), v.numel(), v.dtype)
+            if key not in staged:
+                staged[key] = batch.add(v.contiguous())
+            return staged[key]
+
+        out = self._to_host(npy)
+        batch.finish()
+
+        def fin(v):
+            return v.numpy() if isinstance(v, torch.Tensor) else v
+
+        return out._to_host(fin)
+
+    def _to_host(self, npy) -> "DistShard":
 
         def ps(p):
             return SortedPointSet(level=p.level, points=npy(p.points), charges=npy(p.charges),
@@ -448,11 +471,45 @@ def _shard_csr(bm: torch.Tensor, offset: int, last: bool) -> torch.Tensor:
     return x if last else x[:-1]
 
 
+class PhaseTimer:
+    """CUDA events at the partitioned build's phase boundaries, on the
+    current stream of the driven rank's device (collectives issued through
+    torch.distributed order that stream after their completion).  `ms()`
+    synchronises and returns {phase: ms}; phases repeated over several
+    builds accumulate."""
+
+    def __init__(self):
+        self.marks = []  # (name, event) in order
+
+    def mark(self, name: str) -> None:
+        e = torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.marks.append((name, e))
+
+    def ms(self) -> dict:
+        out = {}
+        if not self.marks:
+            return out
+        self.marks[-1][1].synchronize()
+        for (_, a), (name, b) in zip(self.marks, self.marks[1:]):
+            if name != "start":
+                out[name] = out.get(name, 0.0) + a.elapsed_time(b)
+        return out
+
+
+def _mark(timer, name):
+    if timer is not None:
+        timer.mark(name)
+
+
 def build_all_distributed(shards: list, max_level: int, comm: Comm, ops=None,
-                          pbits: int | None = None, exchange: str | None = None) -> list:
+                          pbits: int | None = None, exchange: str | None = None,
+                          timer: PhaseTimer | None = None) -> list:
     """Partitioned build.  `shards[i] = (src, charges, recv)` of the rank
     comm.ranks[i]: device tensors, index-contiguous pieces of the global
-    arrays in rank order.  Returns one DistShard per driven rank."""
+    arrays in rank order.  Returns one DistShard per driven rank.  `timer`
+    (optional, one driven rank) records the phase boundaries."""
+    _mark(timer, "start")
     check_level(max_level)
     if max_level < 2:
         raise DomainError("the partitioned build needs max_level >= 2")
@@ -475,13 +532,16 @@ def build_all_distributed(shards: list, max_level: int, comm: Comm, ops=None,
     hists = comm.allreduce_sum(hists)
     bin_rank = cut_bins(hists[0], P)
     windows = key_windows(bin_rank, P, L, pb)
+    _mark(timer, "partition (histogram, all-reduce, cut)")
     exchange = exchange or os.environ.get("FMMB_DIST_EXCHANGE", "a2a")
     if exchange == "peer":  # 3'. fused pack + exchange over peer memory
         return _finish(shards, L, comm, ops, P, dev, gb, windows,
-                       _exchange_peer(shards, L, comm, ops, P, pb, bin_rank, gb, dev))
+                       _exchange_peer(shards, L, comm, ops, P, pb, bin_rank, gb, dev, timer),
+                       timer)
     # 3. pack + exchange
     packs = [ops.part_pack(s[0], s[1], s[2], L, pb, bin_rank, P, gb[i][0], gb[i][1])
              for i, s in enumerate(shards)]
+    _mark(timer, "pack")
 
     def split(t, cnts):
         out, at = [], 0
@@ -510,11 +570,14 @@ def build_all_distributed(shards: list, max_level: int, comm: Comm, ops=None,
         received.append({"sxyz": _cat(ex["sxyz"][i]), "sgid": _cat(ex["sgid"][i]),
                          "rxyz": _cat(ex["rxyz"][i]), "rgid": _cat(ex["rgid"][i]),
                          "sq": _cat(ex["sq"][i]) if with_q else None,
-                         "sent_points": sent + sent_r})
-    return _finish(shards, L, comm, ops, P, dev, gb, windows, received)
+                         "sent_points": sent + sent_r,
+                         # payload bytes leaving this rank: xyz + gid (+ q) per point
+                         "sent_bytes": sent * (40 if with_q else 32) + sent_r * 32})
+    _mark(timer, "exchange (all-to-all)")
+    return _finish(shards, L, comm, ops, P, dev, gb, windows, received, timer)
 
 
-def _exchange_peer(shards, L, comm, ops, P, pb, bin_rank, gb, dev) -> list:
+def _exchange_peer(shards, L, comm, ops, P, pb, bin_rank, gb, dev, timer=None) -> list:
     """Fused pack + exchange: counts, one all-gather of them, receive arrays
     sized and shared, then every rank stores its points straight into the
     destinations' arrays (fmmb_part_pack_peer) -- no send buffers, no
@@ -538,7 +601,10 @@ def _exchange_peer(shards, L, comm, ops, P, pb, bin_rank, gb, dev) -> list:
                      "rgid": torch.empty(m_in, **i64)})
         offs.append((soff, roff))
         c = cnts[i]
-        received.append({"sent_points": sum(c[d] + c[P + d] for d in range(P) if d != r)})
+        received.append({"sent_points": sum(c[d] + c[P + d] for d in range(P) if d != r),
+                         "sent_bytes": sum(c[d] * (40 if with_q else 32) + c[P + d] * 32
+                                           for d in range(P) if d != r)})
+    _mark(timer, "pack (counts, receive tables)")
     tables = comm.peer_tables(bufs)
     for i, s in enumerate(shards):
         ops.part_pack_peer(s[0], s[1], s[2], L, pb, bin_rank, P, gb[i][0], gb[i][1], tables[i],
@@ -546,10 +612,11 @@ def _exchange_peer(shards, L, comm, ops, P, pb, bin_rank, gb, dev) -> list:
     comm.peer_barrier()
     for i in range(len(shards)):
         received[i].update(bufs[i])
+    _mark(timer, "exchange (peer stores)")
     return received
 
 
-def _finish(shards, L, comm, ops, P, dev, gb, windows, received) -> list:
+def _finish(shards, L, comm, ops, P, dev, gb, windows, received, timer=None) -> list:
     """Local sort, global occupancy, owned lists, global offsets (steps 4-7)."""
     nd = len(comm.ranks)
     results = []
@@ -561,11 +628,14 @@ def _finish(shards, L, comm, ops, P, dev, gb, windows, received) -> list:
         ss, sr, bmp = ops.dist_sort(rv["sxyz"], rv["sq"], rv["sgid"], rv["rxyz"], rv["rgid"], L)
         sorted_sets.append((ss, sr))
         bmps.append(bmp)
-        results.append({"sent_points": rv["sent_points"]})
+        results.append({"sent_points": rv["sent_points"], "sent_bytes": rv.get("sent_bytes", 0)})
+    _mark(timer, "local sort")
     # 5. global occupancy
     gbmps = comm.allreduce_sum(bmps)
+    _mark(timer, "occupancy all-reduce")
     # 6. owned lists
     lists = [ops.dist_lists(gbmps[i], L, *windows[r]) for i, r in enumerate(comm.ranks)]
+    _mark(timer, "owned lists")
     # 7. global offsets from every rank's shard sizes
     def stats(i):  # host-known sizes (a CSR's last bookmark is its list length)
         ss, sr = sorted_sets[i]
@@ -576,6 +646,7 @@ def _finish(shards, L, comm, ops, P, dev, gb, windows, received) -> list:
         return torch.tensor([int(x) for x in v], dtype=torch.int64, device=dev[i])
 
     allst = comm.all_gather([stats(i) for i in range(nd)])
+    _mark(timer, "offsets (all-gather)")
     out = []
     for i, r in enumerate(comm.ranks):
         st = torch.stack([t.cpu() for t in allst[i]])  # (P, 3 + L - 1)
