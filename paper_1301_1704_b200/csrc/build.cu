@@ -537,12 +537,20 @@ fmmb_status sort_onesweep(fmmb_handle_t h, const double* src, const double* q, i
   return FMMB_OK;
 }
 
-// E2/E4 write pass (warp per receiver parent, grid-stride)
+// E2/E4 write pass (warp per receiver parent, grid-stride).  `sparse`: the
+// finest level's rows average well under the 189 entries of a full window
+// (surfaces, clustered inputs) -- the member-compacting variant visits only
+// the chunks holding occupied members (c3: 0.56 vs 0.64 ms; the dense
+// variant keeps c2 at 1.09 ms)
 inline void launch_lists_write(fmmb_handle_t h, const ListsParams& lp, const ListsLayout* lay,
-                               int64_t nwork_cap, cudaStream_t s) {
+                               int64_t nwork_cap, bool sparse, cudaStream_t s) {
   const int lgrid = (int)std::max<int64_t>(
       1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * 16));
-  k_lists_write<<<lgrid, kLThreads, 0, s>>>(lp, lay);
+  if (sparse) k_lists_write<true><<<lgrid, kLThreads, 0, s>>>(lp, lay);
+  else k_lists_write<false><<<lgrid, kLThreads, 0, s>>>(lp, lay);
+}
+inline bool lists_sparse(int64_t e4_rows_entries, int64_t rows) {
+  return rows > 0 && e4_rows_entries < 120 * rows;
 }
 
 // Multi-GPU sort phase extras: global indices of the local points and the
@@ -918,7 +926,8 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     }
     if (ev) cudaEventRecord(ev[4], s);
     fmmb_trace_point(h, "host: list arena (s)", s);
-    launch_lists_write(h, lp, (const ListsLayout*)W(o_lay), nwork_cap, s);
+    launch_lists_write(h, lp, (const ListsLayout*)W(o_lay), nwork_cap,
+                       lists_sparse(L >= 2 ? hp->seg_totals[L] : 0, kr), s);
     ++launches;
     fmmb_trace_point(h, "lists write (s)", s);
     if (ev) cudaEventRecord(ev[5], s);  // the write kernel alone (before the side join)

@@ -377,7 +377,8 @@ extern "C" fmmb_status fmmb_dist_lists(fmmb_handle_t h, const uint64_t* gbmp, in
     lp.ranks_out[k] = (int64_t*)(arena_b + b_r[k]);
     lp.codes_out[k] = (int16_t*)(arena_b + b_c[k]);
   }
-  launch_lists_write(h, lp, glay, h1.lay.work_off[L + 1], s);
+  launch_lists_write(h, lp, glay, h1.lay.work_off[L + 1],
+                     lists_sparse(L >= 2 ? segt[L] : 0, h1.lay.r_hi[L] - h1.lay.r_lo[L]), s);
   ++h->launches;
 
   memset(out, 0, sizeof(*out));

@@ -340,6 +340,7 @@ __constant__ CandTable kCand = CandTable();
 struct ListsSmem {  // per-CTA copies of the tables (lane-divergent lookups)
   uint8_t order[48][32];
   uint32_t cand[28 * 8];
+  uint32_t slot[kLWarps][2][32];  // per warp: occupied window members, compacted
 };
 __device__ __forceinline__ void load_tables(ListsSmem& t) {
   for (int i = threadIdx.x; i < 48 * 32 / 4; i += blockDim.x)
@@ -354,16 +355,16 @@ __device__ __forceinline__ void load_tables(ListsSmem& t) {
 // near-and-occupied lanes and the chunk's occupied prefix (shared by the
 // rows), and every occupied lane issues ONE rank store (to E2 or E4).
 template <bool E4, bool E2>
-__device__ __forceinline__ void write_rows(uint32_t rm, const uint32_t (&meta)[7],
+__device__ __forceinline__ void write_rows(uint32_t rm, int nch, const uint32_t (&meta)[7],
                                            const uint32_t (&rank)[7], int64_t* __restrict__ r4,
                                            int16_t* __restrict__ c4, int64_t* __restrict__ r2) {
   const unsigned lt = lanemask_lt();
-  uint32_t occ_lt[7], occ_n[7];
+  uint32_t oc[7];  // occupied lanes of the chunk: below this lane | total << 8
 #pragma unroll
   for (int ch = 0; ch < 7; ++ch) {
+    if (ch >= nch) break;  // warp-uniform
     const unsigned ob = ballot_full(meta[ch] & 1u);
-    occ_lt[ch] = __popc(ob & lt);
-    occ_n[ch] = __popc(ob);
+    oc[ch] = __popc(ob & lt) | (__popc(ob) << 8);
   }
   uint32_t rbits = rm;
   while (rbits) {
@@ -372,12 +373,13 @@ __device__ __forceinline__ void write_rows(uint32_t rm, const uint32_t (&meta)[7
     const int crw = (cr & 1) + 7 * ((cr >> 1) & 1) + 49 * ((cr >> 2) & 1);
 #pragma unroll
     for (int ch = 0; ch < 7; ++ch) {
+      if (ch >= nch) break;  // warp-uniform: chunks past the occupied members
       const uint32_t m = meta[ch];
       const uint32_t occ = m & 1u;
       const uint32_t near = (m >> (1 + cr)) & occ;
       const unsigned nb = ballot_full(near);
       const uint32_t a2 = __popc(nb & lt), n2 = __popc(nb);
-      const uint32_t a4 = occ_lt[ch] - a2, n4 = occ_n[ch] - n2;
+      const uint32_t a4 = (oc[ch] & 0xFFu) - a2, n4 = (oc[ch] >> 8) - n2;
       if (E2 && E4) {
         int64_t* dst = near ? r2 + a2 : r4 + a4;
         st_rank(occ, dst, (int64_t)rank[ch]);
@@ -401,8 +403,9 @@ __device__ __forceinline__ void write_rows(uint32_t rm, const uint32_t (&meta)[7
 // member in key order (table, no sort); chunk ch covers members 4ch..4ch+3
 // (lane / 8) and their 8 children (lane % 8): occupancy, source rank, the
 // near bits over the 8 child receivers and the code base, once per P.
+template <bool COMPACT>
 __device__ __forceinline__ void write_parent(const ListsParams& p, const ListsLayout& lay,
-                                             const ListsSmem& t, int L, int l, int64_t j,
+                                             ListsSmem& t, int L, int l, int64_t j,
                                              int lane) {
   const unsigned FULL = 0xffffffffu;
   const int c = lane & 7;
@@ -430,14 +433,39 @@ __device__ __forceinline__ void write_parent(const ListsParams& p, const ListsLa
       }
   }
   if (!own) return;
-  // per chunk: meta = occ | near-over-cr (8 bits) << 1 | code base << 9
+  // occupied members compacted in key order (sparse windows -- surfaces,
+  // deep levels -- visit ceil(members / 4) chunks instead of 7); per chunk:
+  // meta = occ | near-over-cr (8 bits) << 1 | code base << 9
+  const unsigned occs = __ballot_sync(FULL, sm != 0u);
+  const int nocc = COMPACT ? __popc(occs) : 28;
+  // interior with all 27 members occupied: the compacted order is the lane order
+  const bool dense = !COMPACT || occs == 0x7FFFFFFu;
+  uint32_t* sw = t.slot[threadIdx.x >> 5][0];
+  uint32_t* sf = t.slot[threadIdx.x >> 5][1];
+  if (!dense) {
+    __syncwarp();  // the previous parent's reads are done
+    if (sm) {
+      const int at = __popc(occs & lanemask_lt());
+      sw[at] = sm | ((uint32_t)o << 8);
+      sf[at] = sfirst;
+    }
+    __syncwarp();
+  }
+  const int nch = (nocc + 3) >> 2;
   const uint32_t slot_word = sm | ((uint32_t)o << 8);
   uint32_t meta[7], rank[7];
 #pragma unroll
   for (int ch = 0; ch < 7; ++ch) {
     const int slot = 4 * ch + (lane >> 3);
-    const uint32_t v = __shfl_sync(FULL, slot_word, slot);
-    const uint32_t f = __shfl_sync(FULL, sfirst, slot);
+    const bool in = slot < nocc;  // (!COMPACT: slots >= 27 are the o = 27 lanes)
+    uint32_t v, f;
+    if (dense) {
+      v = __shfl_sync(FULL, slot_word, slot);
+      f = __shfl_sync(FULL, sfirst, slot);
+    } else {
+      v = in ? sw[slot] : (27u << 8);
+      f = in ? sf[slot] : 0u;
+    }
     const uint32_t smk = v & 0xFFu;
     const uint32_t tv = t.cand[(v >> 8) * 8 + c];
     const bool occ = (smk >> c) & 1u;  // (unused / out-of-grid members: smk = 0)
@@ -452,19 +480,22 @@ __device__ __forceinline__ void write_parent(const ListsParams& p, const ListsLa
     const int64_t w2 = __ldg(p.bm[0] + rf);
     if (l >= 2) {
       const int64_t w4 = __ldg(p.bm[l] + rf);
-      write_rows<true, true>(own, meta, rank, r4 + w4, c4 + w4, r2 + w2);
+      write_rows<true, true>(own, nch, meta, rank, r4 + w4, c4 + w4, r2 + w2);
     } else {
-      write_rows<false, true>(own, meta, rank, nullptr, nullptr, r2 + w2);
+      write_rows<false, true>(own, nch, meta, rank, nullptr, nullptr, r2 + w2);
     }
   } else {
     const int64_t w4 = __ldg(p.bm[l] + rf);
-    write_rows<true, false>(own, meta, rank, r4 + w4, c4 + w4, nullptr);
+    write_rows<true, false>(own, nch, meta, rank, r4 + w4, c4 + w4, nullptr);
   }
 }
 
+// COMPACT: occupied window members compacted first (sparse levels; the host
+// picks it from the count pass's entries per row), else the dense layout
 #ifndef FMMB_LW_MINB
 #define FMMB_LW_MINB 4
 #endif
+template <bool COMPACT>
 __global__ void __launch_bounds__(kLThreads, FMMB_LW_MINB)
     k_lists_write(const __grid_constant__ ListsParams p, const ListsLayout* __restrict__ glay) {
   __shared__ ListsLayout lay;
@@ -484,7 +515,7 @@ __global__ void __launch_bounds__(kLThreads, FMMB_LW_MINB)
       if (lane == 0 && p.ktot[0]) p.ranks_out[0][p.bm[0][0]] = 0;
       continue;
     }
-    write_parent(p, lay, tab, L, l, j, lane);
+    write_parent<COMPACT>(p, lay, tab, L, l, j, lane);
   }
 }
 
