@@ -59,7 +59,55 @@ struct BucketGeo {
   int qrec;       // source records carry the charge ({x, y, z, q}) and the source
                   // index goes to the idx side array at the same slot; else the
                   // record carries the index and k_gather_q sorts the charges
+  int eb;         // qrec: bits per coordinate exponent of the index embedding
+                  // (0: none; see rec_embed)
 };
+
+// Source records {x, y, z, q} have no room for the input index, but a
+// coordinate v in [2^-(2^eb), 1) is fully described by its 52-bit mantissa
+// and e = -1 - floor(log2 v) < 2^eb: the record then stores the mantissas
+// and moves the three sign+exponent fields (36 bits) into a payload of
+// cbits index bits + 3 eb exponent bits, flagged by x's sign bit and bit 52
+// (raw coordinates with that pattern are negative: a DomainError input).
+// Points with any coordinate outside that range (rare: 3 / 256 of uniform
+// points at eb = 3) keep raw coordinates and the idx side store.
+__device__ __forceinline__ bool rec_embed(double& x, double& y, double& z, uint32_t ci,
+                                          const BucketGeo& g) {
+  if (!g.eb) return false;
+  const uint64_t lo = (uint64_t)(1023 - (1 << g.eb)) << 52;  // bits of 2^-(2^eb)
+  const uint64_t span = (1023ull << 52) - lo;                 // up to 1.0 (excl.)
+  const uint64_t bx = (uint64_t)__double_as_longlong(x), by = (uint64_t)__double_as_longlong(y),
+                 bz = (uint64_t)__double_as_longlong(z);
+  if (bx - lo >= span || by - lo >= span || bz - lo >= span) return false;
+  const uint64_t m52 = (1ull << 52) - 1ull;
+  const uint64_t ex = 1022 - (bx >> 52), ey = 1022 - (by >> 52), ez = 1022 - (bz >> 52);
+  const uint64_t pay = (uint64_t)ci | (ex << g.cbits) | (ey << (g.cbits + g.eb)) |
+                       (ez << (g.cbits + 2 * g.eb));  // < 2^34
+  x = __longlong_as_double((long long)((1ull << 63) | ((((pay & 0x3FFull) << 1) | 1ull) << 52) |
+                                       (bx & m52)));
+  y = __longlong_as_double((long long)((((pay >> 10) & 0xFFFull) << 52) | (by & m52)));
+  z = __longlong_as_double((long long)((((pay >> 22) & 0xFFFull) << 52) | (bz & m52)));
+  return true;
+}
+
+// inverse of rec_embed on a source record: restores x, y, z, returns the
+// index; false (and nothing touched) for a raw record
+__device__ __forceinline__ bool rec_extract(double* r, uint32_t& ci, const BucketGeo& g) {
+  const uint64_t bx = (uint64_t)__double_as_longlong(r[0]);
+  if (!g.eb || !(bx >> 63) || !((bx >> 52) & 1ull)) return false;
+  const uint64_t by = (uint64_t)__double_as_longlong(r[1]), bz = (uint64_t)__double_as_longlong(r[2]);
+  const uint64_t m52 = (1ull << 52) - 1ull;
+  const uint64_t pay = ((bx >> 53) & 0x3FFull) | (((by >> 52) & 0xFFFull) << 10) |
+                       (((bz >> 52) & 0xFFFull) << 22);
+  const uint64_t em = (1ull << g.eb) - 1ull;
+  const uint64_t ex = (pay >> g.cbits) & em, ey = (pay >> (g.cbits + g.eb)) & em,
+                 ez = (pay >> (g.cbits + 2 * g.eb)) & em;
+  ci = (uint32_t)(pay & ((1ull << g.cbits) - 1ull));
+  r[0] = __longlong_as_double((long long)(((1022 - ex) << 52) | (bx & m52)));
+  r[1] = __longlong_as_double((long long)(((1022 - ey) << 52) | (by & m52)));
+  r[2] = __longlong_as_double((long long)(((1022 - ez) << 52) | (bz & m52)));
+  return true;
+}
 
 __host__ inline int ceil_log2(int64_t v) {
   int b = 0;
@@ -617,8 +665,10 @@ __global__ void __launch_bounds__(kSThreads, 1)
       // in k_gather_q): one 32-B store
       const bool sq = qrec && i < n;
       const double w = sq ? xyz[3 * kSRows + tid] : __longlong_as_double(i < n ? i : i - n);
-      st_v4f64(rec + 4 * (size_t)dst, xyz[3 * tid], xyz[3 * tid + 1], xyz[3 * tid + 2], w);
-      if (sq) idx[dst] = (uint32_t)i;
+      double x = xyz[3 * tid], y = xyz[3 * tid + 1], z = xyz[3 * tid + 2];
+      const bool emb = sq && rec_embed(x, y, z, (uint32_t)i, g);  // index in the exponents
+      st_v4f64(rec + 4 * (size_t)dst, x, y, z, w);
+      if (sq && !emb) idx[dst] = (uint32_t)i;
     }
     mbar_arrive(empty + k % kSStages);
   };
@@ -845,14 +895,17 @@ __global__ void __launch_bounds__(kLcThreads)
     for (int i = tid; i < nbins; i += kLcThreads) s_wh[i] = 0;
   __syncthreads();
   for (int j = tid; j < B; j += kLcThreads) {
-    const double* r = s_rec + 4 * j;
+    double* r = s_rec + 4 * j;
+    // combined input index: embedded in a source record's exponents (the
+    // coordinates are restored in place), else the idx side array (qrec),
+    // else the record's last word (index within the set)
+    uint32_t ci;
+    if (g.qrec && set == 0) {
+      if (!rec_extract(r, ci, g)) ci = __ldg(idx + rb + j);
+    } else {
+      ci = (uint32_t)(set ? n + __double_as_longlong(r[3]) : __double_as_longlong(r[3]));
+    }
     const uint64_t key = encode_any<NARROW>(r[0], r[1], r[2], level, grid);
-    // combined input index: source indices from the side array (qrec), else
-    // the record's last word (index within the set)
-    const uint32_t ci = (g.qrec && set == 0)
-                            ? __ldg(idx + rb + j)
-                            : (uint32_t)(set ? n + __double_as_longlong(r[3])
-                                             : __double_as_longlong(r[3]));
     // < span for every valid point; out-of-grid inputs (reported as a DomainError
     // after the build) are clamped so they cannot index outside the bucket
     uint64_t lk = (key & ((1ull << g.sbits) - 1ull)) - prefix;

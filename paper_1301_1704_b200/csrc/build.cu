@@ -92,6 +92,7 @@ extern "C" fmmb_status fmmb_create(int device, fmmb_handle_t* out) {
     h->overlap = getenv("FMMB_NO_OVERLAP") == nullptr;
     h->early_occ = getenv("FMMB_LATE_OCC") ? 0 : getenv("FMMB_EARLY_OCC") ? 2 : 1;
     h->rec_q = getenv("FMMB_REC_IDX") == nullptr;
+    h->rec_embed = getenv("FMMB_NO_EMBED") == nullptr;
     const char* sc = getenv("FMMB_SCATTER_CTAS");
     h->scatter_ctas = sc ? atoi(sc) : 0;
     h->trace = getenv("FMMB_TRACE") != nullptr;
@@ -369,6 +370,10 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
                         BucketRun& run, cudaStream_t ls, bool early) {
   BucketGeo g = bucket_geo(L, n, m, h->num_sms);
   g.qrec = (q && n > 0 && h->rec_q) ? 1 : 0;
+  // index embedding in the source records' exponents: 34 payload bits hold
+  // the index and three exponents of eb bits (FMMB_NO_EMBED=1: side store only)
+  g.eb = (g.qrec && h->rec_embed) ? std::min(3, (34 - g.cbits) / 3) : 0;
+  if (g.eb < 1) g.eb = 0;
   const int64_t tot = n + m;
   const int64_t nfcap = final_buckets_cap(g, kLcCap);
   const int64_t nrec = spec ? (int64_t)g.nb * kSpecStride : tot;  // record slots

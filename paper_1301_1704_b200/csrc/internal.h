@@ -34,6 +34,7 @@ struct fmmb_handle_s {
                                  // (FMMB_LATE_OCC=1)
   bool rec_q = true;             // source records carry q + idx side store (FMMB_REC_IDX=1:
                                  // records carry the index, charges gathered after the sort)
+  bool rec_embed = true;         // source index in the record's exponents where possible
   int scatter_ctas = 0;          // FMMB_SCATTER_CTAS: cap on the scatter's persistent grid (A/B)
   bool overlap = true;           // FMMB_NO_OVERLAP=1 serialises (A/B)
   bool local_after_count = false;  // FMMB_LOCAL_AFTER=1: local pass after the list count (A/B)
