@@ -284,6 +284,12 @@ FMMB_API fmmb_status fmmb_dist_sort(fmmb_handle_t h, const double* src, const do
                            const int64_t* gid_recv, int level, fmmb_alloc_fn alloc, void* ctx,
                            fmmb_point_set* src_out, fmmb_point_set* recv_out, uint64_t* bmp,
                            void* stream);
+/* fmmb_dist_sort returns once the occupancy bitmap (`bmp`) and the box
+ * counts are final; its local pass (sorted points, permutation, bookmarks)
+ * may still run on the handle's side stream, beside the bitmap all-reduce
+ * and fmmb_dist_lists.  fmmb_dist_join orders `stream` after it: call it
+ * before reading the sorted point sets. */
+FMMB_API fmmb_status fmmb_dist_join(fmmb_handle_t h, void* stream);
 
 /* Lists of one rank from the GLOBAL level-L bitmaps (gbmp, layout as above):
  * receiver rows owned by the key window [key_lo, key_hi) at every level (a

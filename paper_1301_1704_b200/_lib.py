@@ -96,6 +96,7 @@ SIGNATURES = [
     ("fmmb_dist_sort", C.c_int,
      [_p, _p, _p, _i64, _p, _p, _i64, _p, C.c_int, ALLOC_FN, _p, C.POINTER(PointSetC),
       C.POINTER(PointSetC), _p, _p]),
+    ("fmmb_dist_join", C.c_int, [_p, _p]),
     ("fmmb_dist_lists", C.c_int,
      [_p, _p, C.c_int, C.c_uint64, C.c_uint64, ALLOC_FN, _p, C.POINTER(StructuresC), _p]),
     ("fmmb_near_field", C.c_int,

@@ -564,6 +564,7 @@ struct DistSortArgs {
   const int64_t* gid_src;
   const int64_t* gid_recv;
   uint64_t* bmp;
+  bool defer_join;  // leave the local pass running on the side stream (fmmb_dist_join)
 };
 
 template <typename KeyT>
@@ -957,7 +958,11 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
       out->n_st[k] = hp->seg_totals[k];
     }
   }
-  join();  // the caller's stream sees the local pass and heads complete
+  // the caller's stream sees the local pass and heads complete (the
+  // partitioned sort defers this: its bitmap all-reduce and owned lists only
+  // need the occupancy, fmmb_dist_join orders the caller after the rest)
+  const bool deferred = dsa && dsa->defer_join && ls != s;
+  if (!deferred) join();
   fmmb_trace_point(h, "joined (s)", s);
   if (ev) {
     if (!lists) {
@@ -965,7 +970,8 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
       cudaEventRecord(ev[5], s);
     }
   }
-  cudaFreeAsync(ws, s);
+  // (deferred: the heads pass on the side stream still reads the directory)
+  cudaFreeAsync(ws, deferred ? ls : s);
   out->n_launches = launches;
   h->launches = launches;
   cudaError_t ce = cudaGetLastError();

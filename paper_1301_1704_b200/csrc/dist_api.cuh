@@ -193,7 +193,7 @@ extern "C" fmmb_status fmmb_dist_sort(fmmb_handle_t h, const double* src, const 
   if (st != FMMB_OK) return st;
   if (!src_out || !recv_out || !bmp || level < 1) return FMMB_ERR_ARG;
   cudaSetDevice(h->device);
-  DistSortArgs dsa{gid_src, gid_recv, bmp};
+  DistSortArgs dsa{gid_src, gid_recv, bmp, true};
   fmmb_structures tmp;
   cudaStream_t s = (cudaStream_t)stream;
   if (sort_key_bits(level) <= 32)
@@ -207,6 +207,13 @@ extern "C" fmmb_status fmmb_dist_sort(fmmb_handle_t h, const double* src, const 
     *recv_out = tmp.recv;
   }
   return st;
+}
+
+extern "C" fmmb_status fmmb_dist_join(fmmb_handle_t h, void* stream) {
+  FMMB_GUARD(h);
+  cudaSetDevice(h->device);
+  if (h->side) cudaStreamWaitEvent((cudaStream_t)stream, (cudaEvent_t)h->ev_side, 0);
+  return cuda_status(h, "dist_join");
 }
 
 namespace {

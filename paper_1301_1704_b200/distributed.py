@@ -318,6 +318,12 @@ class DeviceOps:
         return (_point_set_from_c(so, alloc, level, q is not None),
                 _point_set_from_c(ro, alloc, level, False), bmp)
 
+    def dist_join(self, device):
+        """Order the current stream after the local pass of the last dist_sort."""
+        dev = _lib.device_of(device)
+        h = _lib.handle(dev)
+        _lib.check(_lib.load().fmmb_dist_join(h, _lib.stream_of(dev)), h)
+
     def dist_lists(self, gbmp, level, key_lo, key_hi):
         dev = _lib.device_of(gbmp.device)
         h = _lib.handle(dev)
@@ -358,12 +364,16 @@ def cut_bins(hist: torch.Tensor, nranks: int) -> torch.Tensor:
     """Rank of every histogram bin: contiguous bin ranges with balanced point
     counts, rank(b) = min(P-1, floor(P * points-before-b / total)).  A pure
     function of the all-reduced histogram, so every rank computes the same."""
-    h = hist.to(torch.int64)
-    excl = torch.cumsum(h, 0) - h
+    # on the host: one small read-back instead of a chain of device ops and
+    # syncs (the all-reduced histogram has <= 2^14 bins)
+    h = hist.detach().to("cpu", torch.int64).numpy()
+    excl = np.cumsum(h) - h
     tot = int(h.sum())
     if tot == 0:
-        return torch.zeros_like(h)
-    return torch.clamp((excl * nranks) // tot, max=nranks - 1)
+        out = np.zeros_like(h)
+    else:
+        out = np.minimum((excl * nranks) // tot, nranks - 1)
+    return torch.from_numpy(out).to(hist.device)
 
 
 def key_windows(bin_rank: torch.Tensor, nranks: int, level: int, pbits: int) -> list:
@@ -530,8 +540,9 @@ def build_all_distributed(shards: list, max_level: int, comm: Comm, ops=None,
     # 2. histogram -> cut
     hists = [ops.part_histogram(s[0], s[2], L, pb) for s in shards]
     hists = comm.allreduce_sum(hists)
-    bin_rank = cut_bins(hists[0], P)
-    windows = key_windows(bin_rank, P, L, pb)
+    br_host = cut_bins(hists[0].cpu(), P)
+    windows = key_windows(br_host, P, L, pb)
+    bin_rank = br_host.to(dev[0], non_blocking=True)
     _mark(timer, "partition (histogram, all-reduce, cut)")
     exchange = exchange or os.environ.get("FMMB_DIST_EXCHANGE", "a2a")
     if exchange == "peer":  # 3'. fused pack + exchange over peer memory
@@ -635,6 +646,9 @@ def _finish(shards, L, comm, ops, P, dev, gb, windows, received, timer=None) -> 
     _mark(timer, "occupancy all-reduce")
     # 6. owned lists
     lists = [ops.dist_lists(gbmps[i], L, *windows[r]) for i, r in enumerate(comm.ranks)]
+    for i in range(nd):  # the local passes ran beside the all-reduce and the lists
+        if hasattr(ops, "dist_join"):
+            ops.dist_join(dev[i])
     _mark(timer, "owned lists")
     # 7. global offsets from every rank's shard sizes
     def stats(i):  # host-known sizes (a CSR's last bookmark is its list length)
