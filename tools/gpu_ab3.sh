@@ -1,0 +1,13 @@
+set -x
+mkdir -p gpurun_out/ab3
+B="python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e --no-nf --workload"
+for w in c2 c4; do
+  timeout 300 $B $w > gpurun_out/ab3/base_$w.log 2>&1
+  FMMB_LOCAL_AFTER=1 timeout 300 $B $w > gpurun_out/ab3/after_$w.log 2>&1
+  FMMB_SIDE_PRIO=1 timeout 300 $B $w > gpurun_out/ab3/prio_$w.log 2>&1
+  FMMB_LC_PER_SM=2 timeout 300 $B $w > gpurun_out/ab3/lc2_$w.log 2>&1
+  FMMB_SIDE_PRIO=1 FMMB_LC_PER_SM=2 timeout 300 $B $w > gpurun_out/ab3/prio_lc2_$w.log 2>&1
+done
+for f in gpurun_out/ab3/*.log; do python -c "
+import json
+d=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', round(d['ms_per_step'],3), {k: round(v,3) for k,v in d['phases_ms'].items()})"; done
