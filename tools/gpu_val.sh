@@ -1,0 +1,14 @@
+# round validation: smoke, full GPU suite, official bench line, reference arm, c1-c4 lines
+set -x
+mkdir -p gpurun_out/val
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/val/smoke.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q 2>&1 | tail -5 > gpurun_out/val/pytest_all.log
+timeout 900 python bench.py > gpurun_out/val/bench_official.log 2>&1
+B="python bench.py --steps 10 --warmup 3 --no-cpu --no-e2e --no-nf"
+for w in c1 c3 c4; do timeout 300 $B --workload $w > gpurun_out/val/$w.log 2>&1; done
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/val/launches_c2.csv python bench.py --steps 2 --warmup 3 --no-cpu --no-e2e --no-nf > /dev/null 2>&1
+cat gpurun_out/val/smoke.log gpurun_out/val/pytest_all.log
+tail -1 gpurun_out/val/bench_official.log | cut -c1-400
+for f in gpurun_out/val/c?.log; do python -c "
+import json
+d=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', round(d['ms_per_step'],3), {k: round(v,3) for k,v in d['phases_ms'].items()})"; done
