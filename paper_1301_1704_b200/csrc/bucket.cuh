@@ -371,21 +371,35 @@ __global__ void __launch_bounds__(256)
     c = bstart[b + 1] - bstart[b];
     ns = 1;
     if (refined && needs_refine(g, c, cap)) {  // greedy groups of consecutive sub-bins
+      // (sub-bin counts streamed 4 at a time, group ids stored 4 per word)
       const uint32_t* f = fine + (size_t)b * kRefBins;
+      uint8_t* gt = o.gtab + (size_t)b * kRefBins;
       uint32_t acc = 0, grp = 0;
       int run = 0;
-      for (int sb = 0; sb < nsub; ++sb) {
-        const uint32_t v = f[sb];
-        if (v > cap) atomicOr(o.fail, 1u);
-        if ((acc + v > cap && acc > 0) || run == max_run) {
-          ++grp;
-          acc = 0;
-          run = 0;
+      bool over = false;
+      for (int q4 = 0; q4 < (nsub + 3) / 4; ++q4) {
+        const uint4 v4 = nsub >= 4 ? __ldg(reinterpret_cast<const uint4*>(f) + q4)
+                                   : make_uint4(f[0], nsub > 1 ? f[1] : 0u, 0u, 0u);
+        const uint32_t vv[4] = {v4.x, v4.y, v4.z, v4.w};
+        uint32_t packed = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (4 * q4 + e >= nsub) break;
+          const uint32_t v = vv[e];
+          over |= v > cap;
+          if ((acc + v > cap && acc > 0) || run == max_run) {
+            ++grp;
+            acc = 0;
+            run = 0;
+          }
+          acc += v;
+          ++run;
+          packed |= (grp & 0xFFu) << (8 * e);
         }
-        acc += v;
-        ++run;
-        o.gtab[(size_t)b * kRefBins + sb] = (uint8_t)grp;
+        if (nsub >= 4) reinterpret_cast<uint32_t*>(gt)[q4] = packed;
+        else for (int e = 0; e < nsub; ++e) gt[e] = (uint8_t)(packed >> (8 * e));
       }
+      if (over) atomicOr(o.fail, 1u);
       ns = grp + 1;
     }
   }
@@ -426,24 +440,41 @@ __global__ void __launch_bounds__(256)
     o.cursor[(size_t)fb * kCursorStride] = bstart[b];
     return;
   }
+  // the same greedy walk again, emitting each group's start, key range and
+  // cursor (no read-back of the group table)
   const uint32_t* f = fine + (size_t)b * kRefBins;
   const int sh = g.shift - R;
   uint32_t start = bstart[b];
-  int first = 0;
-  for (int sb = 0; sb <= nsub; ++sb) {
-    const bool end = sb == nsub || o.gtab[(size_t)b * kRefBins + sb] !=
-                                       o.gtab[(size_t)b * kRefBins + first];
-    if (end) {
-      const uint32_t fid = fb + o.gtab[(size_t)b * kRefBins + first];
-      uint32_t cnt = 0;
-      for (int k = first; k < sb; ++k) cnt += f[k];
-      o.bstart_f[fid] = start;
-      o.desc[fid] = BDesc{lo + ((uint64_t)first << sh), ((uint64_t)(sb - first) << sh) | (set << 63)};
-      o.cursor[(size_t)fid * kCursorStride] = start;
-      start += cnt;
-      first = sb;
+  uint32_t acc = 0, grp = 0;
+  int run = 0, first = 0;
+  auto emit = [&](int end) {
+    const uint32_t fid = fb + grp;
+    o.bstart_f[fid] = start;
+    o.desc[fid] = BDesc{lo + ((uint64_t)first << sh), ((uint64_t)(end - first) << sh) | (set << 63)};
+    o.cursor[(size_t)fid * kCursorStride] = start;
+    start += acc;
+  };
+  for (int q4 = 0; q4 < (nsub + 3) / 4; ++q4) {
+    const uint4 v4 = nsub >= 4 ? __ldg(reinterpret_cast<const uint4*>(f) + q4)
+                               : make_uint4(f[0], nsub > 1 ? f[1] : 0u, 0u, 0u);
+    const uint32_t vv[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int sb = 4 * q4 + e;
+      if (sb >= nsub) break;
+      const uint32_t v = vv[e];
+      if ((acc + v > cap && acc > 0) || run == max_run) {
+        emit(sb);
+        ++grp;
+        acc = 0;
+        run = 0;
+        first = sb;
+      }
+      acc += v;
+      ++run;
     }
   }
+  emit(nsub);
 }
 
 // ------------------------------------------------ speculative regions ----

@@ -174,3 +174,35 @@ def test_build_all_deep_levels(gpu, ref, n, m, level, seed):
     bs = got.build_seconds
     assert set(bs) >= {"sort_sources", "sort_receivers", "neighbor_table", "level_directory",
                        "stencils"} and all(v >= 0 for v in bs.values())
+
+
+def test_index_embedding_edges_match_reference(gpu, ref):
+    """Source records carry their index in the coordinates' exponent fields
+    when every coordinate lies in [2^-8, 1) (bucket.cuh rec_embed): points on
+    and around the range edges -- 0, -0.0, subnormals, 2^-8 and its neighbours,
+    1 - ulp, exactly 1.0, values above 1 (clamped by the encoder) -- mixed
+    with ordinary points must come out bit-identical to the reference."""
+    rng = np.random.default_rng(5)
+    n, m, L = 6000, 4000, 5
+    src = rng.random((n, 3))
+    recv = rng.random((m, 3))
+    q = rng.normal(size=n)
+    edge = np.array([0.0, -0.0, 5e-324, 2.0**-8, np.nextafter(2.0**-8, 0), np.nextafter(2.0**-8, 1),
+                     2.0**-9, 0.5, np.nextafter(1.0, 0), 1.0, 1.5, 7.25, 2.0**-7, 0.999])
+    k = 0
+    for i in range(0, n, 7):  # every 7th source gets edge values on 1-3 axes
+        for a in range(1 + i % 3):
+            src[i, (a + i) % 3] = edge[k % edge.size]
+            k += 1
+    for i in range(0, m, 11):
+        recv[i, i % 3] = edge[k % edge.size]
+        k += 1
+    want = ref.build_all(src, q, recv, max_level=L)
+    for path in ("auto", "bucket_hist"):
+        gpu._lib.set_sort_path(path)
+        try:
+            got = gpu.build_all(src, q, recv, max_level=L)
+        finally:
+            gpu._lib.set_sort_path("auto")
+        errors = compare_structures(got, want)
+        assert not errors, "\n".join(errors)
