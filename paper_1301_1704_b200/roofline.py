@@ -62,13 +62,16 @@ def build_bytes(c: dict) -> int:
 
 
 def list_write_bytes(c: dict) -> int:
-    """Compulsory bytes of the list write kernel (k_lists<true>): every E2 and
-    E4 entry written once (i64 rank, i16 code), each CSR bookmark and each
-    receiver-parent key read once."""
+    """Compulsory bytes of the list write kernel (k_lists_write) itself: every
+    E2 and E4 entry written once (i64 rank, i16 code), and per receiver parent
+    its key and the first CSR offset of its rows (one per CSR it writes: E4,
+    and E2 at the finest level) read once.  The CSR bookmarks are written by
+    the count pass (k_lists_cscan), not here."""
     L = c["L"]
-    b = 8 * c["e2"] + 8 * (c["kr"] + 1)
+    b = 8 * c["e2"]
     for l in range(2, L + 1):
-        b += 10 * c["s_l"][l] + 8 * (c["kr_l"][l] + 1)
+        b += 10 * c["s_l"][l]
     for l in range(max(1, 2 if L >= 2 else L), L + 1):
-        b += 8 * c["kr_l"].get(l - 1, 0)  # parent keys (levels < 2 are a handful)
+        parents = c["kr_l"].get(l - 1, 0)
+        b += 8 * parents * (1 + (1 if l >= 2 else 0) + (1 if l == L else 0))
     return b
