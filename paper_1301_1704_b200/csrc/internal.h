@@ -26,8 +26,8 @@ struct fmmb_handle_s {
   void* ev_side = nullptr;       // side stream's work done
   void* ev_plan = nullptr;       // early occupancy: refinement plan done (sort stream)
   void* ev_count = nullptr;      // early occupancy: list count done (caller stream)
-  bool scatter_after_count = true;  // early occupancy: scatter waits for the list count
-                                    // (FMMB_SCATTER_EARLY=1: right after the plan)
+  bool scatter_after_count = false;  // early occupancy: scatter waits for the list count
+                                    // (FMMB_SCATTER_AFTER_COUNT=1; default: right after the plan)
   int early_occ = 1;             // occupancy bits from the histogram pass, sort on the side
                                  // stream beside the directory + lists: 1 when the histogram
                                  // pass runs anyway, 2 always (FMMB_EARLY_OCC=1), 0 never
