@@ -1,0 +1,10 @@
+set -x
+mkdir -p gpurun_out/q5
+timeout 1200 python -m pytest tests/test_gpu_northstar.py tests/test_gpu_build_parity.py tests/test_gpu_golden.py tests/test_gpu_distributed.py tests/test_gpu_errors.py -q -x 2>&1 | tail -3 > gpurun_out/q5/pytest.log
+B="python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e --no-nf --workload"
+for w in c3 c2 c4; do timeout 300 $B $w > gpurun_out/q5/$w.log 2>&1; done
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"k_bkt_hist|k_bkt_scan" --csv --log-file gpurun_out/q5/l_c3.csv python tools/profile_build.py c3 1 > /dev/null 2>&1
+cat gpurun_out/q5/pytest.log; python tools/launches.py gpurun_out/q5/l_c3.csv | tail -5
+for f in gpurun_out/q5/c?.log; do python -c "
+import json
+d=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', round(d['ms_per_step'],3), {k: round(v,3) for k,v in d['phases_ms'].items()})"; done
