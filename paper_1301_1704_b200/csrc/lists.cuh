@@ -337,6 +337,41 @@ struct CandTable {
 };
 __constant__ CandTable kCand = CandTable();
 
+// ---- dense windows.  When all 27 window members of a receiver parent are
+// in the grid with all 8 children occupied, and all 8 child receivers are
+// owned (c2: ~85 % of the finest-level parents), every row's output is a
+// fixed sequence: E4 = the 189 candidates outside the child's own window,
+// E2 = the 27 inside, in (member slot, child) order, with consecutive source
+// ranks per member.  The sequences depend only on the window case and the
+// child, so they are tabulated (entry = slot * 8 + child) and a row is
+// written lane = output entry: no ballots, no compaction.
+struct DenseSeq {
+  uint8_t e4[48][8][192];
+  uint8_t e2[48][8][32];
+  constexpr DenseSeq() : e4(), e2() {
+    const WinOrder wo;
+    for (int cs = 0; cs < 48; ++cs)
+      for (int cr = 0; cr < 8; ++cr) {
+        int k4 = 0, k2 = 0;
+        for (int sl = 0; sl < 27; ++sl) {
+          const int o = wo.o[cs][sl];
+          const int off[3] = {o % 3 - 1, (o / 3) % 3 - 1, o / 9 - 1};
+          for (int c = 0; c < 8; ++c) {
+            bool near = true;
+            for (int a = 0; a < 3; ++a) {
+              const int d = 2 * off[a] + ((c >> a) & 1) - ((cr >> a) & 1);
+              near = near && d >= -1 && d <= 1;
+            }
+            if (near) e2[cs][cr][k2++] = (uint8_t)(sl * 8 + c);
+            else e4[cs][cr][k4++] = (uint8_t)(sl * 8 + c);
+          }
+        }
+      }
+  }
+};
+__device__ const DenseSeq kDense = DenseSeq();
+constexpr int kDenseE4 = 189, kDenseE2 = 27;
+
 struct ListsSmem {  // per-CTA copies of the tables (lane-divergent lookups)
   uint8_t order[48][32];
   uint32_t cand[28 * 8];
@@ -433,6 +468,40 @@ __device__ __forceinline__ void write_parent(const ListsParams& p, const ListsLa
       }
   }
   if (!own) return;
+  if (!COMPACT && l >= 2 && own == 0xFFu &&
+      __all_sync(FULL, lane >= 27 || sm == 0xFFu)) {  // dense window (see DenseSeq)
+    const int cs = window_case(P, l - 1);
+    const uint32_t rf = (uint32_t)r0;
+    int64_t* r4 = p.ranks_out[l] + __ldg(p.bm[l] + rf);
+    int16_t* c4 = p.codes_out[l] + __ldg(p.bm[l] + rf);
+    int64_t* r2 = l == L ? p.ranks_out[0] + __ldg(p.bm[0] + rf) : nullptr;
+#pragma unroll 1
+    for (int cr = 0; cr < 8; ++cr) {
+      const int crw = (cr & 1) + 7 * ((cr >> 1) & 1) + 49 * ((cr >> 2) & 1);
+      const uint8_t* q4 = &kDense.e4[cs][cr][0];
+#pragma unroll
+      for (int g = 0; g < 6; ++g) {
+        const int tt = 32 * g + lane;
+        const uint32_t e = __ldg(q4 + (tt < kDenseE4 ? tt : 0));
+        const int sl = (int)(e >> 3), cc = (int)(e & 7u);
+        const uint32_t f = __shfl_sync(FULL, sfirst, sl);
+        const int om = __shfl_sync(FULL, o, sl);
+        if (tt < kDenseE4) {
+          r4[tt] = (int64_t)(f + (uint32_t)cc);
+          c4[tt] = (int16_t)((int)(t.cand[om * 8 + cc] >> 8) - crw);
+        }
+      }
+      r4 += kDenseE4;
+      c4 += kDenseE4;
+      if (r2) {
+        const uint32_t e = __ldg(&kDense.e2[cs][cr][lane < kDenseE2 ? lane : 0]);
+        const uint32_t f = __shfl_sync(FULL, sfirst, (int)(e >> 3));
+        if (lane < kDenseE2) r2[lane] = (int64_t)(f + (e & 7u));
+        r2 += kDenseE2;
+      }
+    }
+    return;
+  }
   // occupied members compacted in key order (sparse windows -- surfaces,
   // deep levels -- visit ceil(members / 4) chunks instead of 7); per chunk:
   // meta = occ | near-over-cr (8 bits) << 1 | code base << 9
