@@ -218,20 +218,25 @@ class Allocator:
     def __init__(self, dev: torch.device):
         self.dev = dev
         blocks: list[torch.Tensor] = []
+        spans: list[tuple[int, int]] = []  # (base address, bytes) of each block
         errors: list[BaseException] = []
         self.blocks = blocks
+        self.spans = spans
         self._errors = errors
 
         # the closure must not reference `self` (a cycle would keep every
         # output block alive until the cyclic GC runs)
         def _alloc(_ctx, nbytes):
             try:
-                t = torch.empty(max(int(nbytes), 1), dtype=torch.uint8, device=dev)
+                nb = max(int(nbytes), 1)
+                t = torch.empty(nb, dtype=torch.uint8, device=dev)
             except BaseException as e:  # noqa: BLE001 - reported after the call
                 errors.append(e)
                 return None
             blocks.append(t)
-            return t.data_ptr()
+            ptr = t.data_ptr()
+            spans.append((ptr, nb))
+            return ptr
 
         self.fn = ALLOC_FN(_alloc)
 
@@ -251,22 +256,21 @@ class Allocator:
         block and dtype, when the block and the offset are `size`-aligned:
         one slicing op per output view instead of three."""
         cache = self.__dict__.setdefault("_typed", {})
-        for i, b in enumerate(self.blocks):
-            base = b.data_ptr()
-            n = b.numel()
+        for i, (base, n) in enumerate(self.spans):
             if base <= ptr < base + n or ptr == base:
                 off = ptr - base
                 if off % size or n % size:
                     return None
                 t = cache.get((i, tdt))
                 if t is None:
-                    t = b.view(tdt)
+                    t = self.blocks[i].view(tdt)
                     cache[(i, tdt)] = t
                 return t, off // size
         raise NativeError(f"pointer {ptr:#x} is not in any allocated block")
 
 
 _SIZES = {"f8": 8, "i8": 8, "u8": 8, "i2": 2, "u4": 4, "i4": 4}
+_EMPTY: dict = {}
 _TORCH_DTYPES = {
     "f8": torch.float64, "i8": torch.int64, "u8": torch.uint64, "i2": torch.int16,
     "u4": torch.uint32, "i4": torch.int32,
@@ -277,8 +281,12 @@ def view(alloc: Allocator, ptr: int | None, count: int, dtype: str, shape=None) 
     """Typed device view of `count` elements at `ptr` inside an allocated block."""
     tdt = _TORCH_DTYPES[dtype]
     if not ptr or count == 0:
-        t = torch.empty(0, dtype=tdt, device=alloc.dev)
-        return t.reshape(shape if shape is not None else (0,)) if shape is not None else t
+        key = (alloc.dev, tdt, tuple(shape) if shape is not None else (0,))
+        t = _EMPTY.get(key)  # zero-size views are shared (nothing to alias)
+        if t is None:
+            t = torch.empty(key[2], dtype=tdt, device=alloc.dev)
+            _EMPTY[key] = t
+        return t
     size = _SIZES[dtype]
     tv = alloc.typed(ptr, tdt, size)
     if tv is not None:

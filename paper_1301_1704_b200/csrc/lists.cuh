@@ -61,6 +61,7 @@ __device__ __forceinline__ int lists_lmin(int L) { return L >= 2 ? 2 : L; }
 // rank of `key` among the set bits of (set, level l): boxes with smaller keys
 __device__ inline int64_t level_rank(const ListsParams& p, int set, int l, uint64_t key) {
   const int L = p.level;
+  if (key == 0) return 0;  // (single-GPU windows start at 0: no lookup)
   if (key >= (1ull << (3 * l))) return p.ktot[set * (L + 1) + l];
   const uint64_t* bmp = p.bmp + p.bmp_off[set][l];
   const uint32_t* dir = p.dir + p.bmp_off[set][l];
