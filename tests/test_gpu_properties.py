@@ -70,3 +70,70 @@ def test_full_size_properties(gpu, name):
     st = gpu.build_all_device(s, qq, r, wl.level)
     _check(st, s, r, wl.level)
     assert torch.equal(st.sorted_src.charges, qq[st.sorted_src.permutation])
+
+
+def _flat(st):
+    out = {}
+    for side in ("sorted_src", "sorted_recv"):
+        ps = getattr(st, side)
+        for f in ("points", "charges", "permutation", "bookmarks", "non_empty_index", "boxes"):
+            v = getattr(ps, f)
+            if v is not None:
+                out[f"{side}.{f}"] = v
+    out["nb"] = st.neighbor_table.neighbor_bookmark
+    out["nl"] = st.neighbor_table.neighbor_list
+    for l, v in st.directory.src_boxes.items():
+        out[f"ds{l}"] = v
+    for l, v in st.directory.recv_boxes.items():
+        out[f"dr{l}"] = v
+    for l in st.stencils.ranks:
+        out[f"sb{l}"] = st.stencils.bookmark[l]
+        out[f"sr{l}"] = st.stencils.ranks[l]
+        out[f"sc{l}"] = st.stencils.codes[l]
+    return out
+
+
+def test_wide_index_embedding_matches_onesweep(gpu):
+    """n + m = 2^26 + 2^20: the combined index needs 27 bits, so the source
+    records embed it with 2-bit exponents (coordinates in [2^-4, 1), the rest
+    take the side store) -- every output array equals the Onesweep path's,
+    which never builds records."""
+    dev = torch.device("cuda", 0)
+    g = torch.Generator(device=dev)
+    g.manual_seed(17)
+    n, m, L = 2**26, 2**20, 7
+    src = torch.rand((n, 3), generator=g, device=dev, dtype=torch.float64)
+    src[::97, 1] *= 0.05  # plenty of coordinates below 2^-4 (side-store escapes)
+    recv = torch.rand((m, 3), generator=g, device=dev, dtype=torch.float64)
+    q = torch.randn(n, generator=g, device=dev, dtype=torch.float64)
+    a = _flat(gpu.build_all_device(src, q, recv, L))
+    gpu._lib.set_sort_path("onesweep")
+    try:
+        b = _flat(gpu.build_all_device(src, q, recv, L))
+    finally:
+        gpu._lib.set_sort_path("auto")
+    assert a.keys() == b.keys()
+    for k in a:
+        assert a[k].dtype == b[k].dtype and a[k].shape == b[k].shape, k
+        assert torch.equal(a[k].view(torch.uint8), b[k].view(torch.uint8)), k
+
+
+def test_phase_trace_and_partitioned_timer(gpu):
+    """The FMMB_TRACE timeline API answers (empty when the handle was created
+    without it) and the partitioned build's PhaseTimer reports every phase."""
+    from paper_1301_1704_b200 import distributed as D
+
+    dev = torch.device("cuda", 0)
+    assert isinstance(gpu._lib.trace(dev), list)
+    src, q, recv = (torch.from_numpy(a).to(dev) for a in generate(20000, 15000, "uniform", 3))
+    comm = D.SimComm(2)
+    half = (src.shape[0] // 2, recv.shape[0] // 2)
+    shards = [(src[:half[0]], q[:half[0]], recv[:half[1]]),
+              (src[half[0]:], q[half[0]:], recv[half[1]:])]
+    timer = D.PhaseTimer()
+    out = D.build_all_distributed(shards, 5, comm, timer=timer)
+    ph = timer.ms()
+    for k in ("partition (histogram, all-reduce, cut)", "pack", "exchange (all-to-all)",
+              "local sort", "occupancy all-reduce", "owned lists", "offsets (all-gather)"):
+        assert k in ph and ph[k] >= 0.0, k
+    assert len(out) == 2 and sum(int(s.exchanged["sent_bytes"]) for s in out) > 0
