@@ -68,19 +68,23 @@ extern "C" fmmb_status fmmb_create(int device, fmmb_handle_t* out) {
     return FMMB_ERR_CUDA;
   }
   {
-    cudaStream_t side;
+    cudaStream_t side, side_hi;
     cudaEvent_t e[5];
-    // FMMB_SIDE_PRIO=1: the sort stream at the highest priority, so its
-    // pending CTAs (local pass) are dispatched before the list write's
+    // two sort streams: default priority (late occupancy: the local pass
+    // beside the lists) and the highest priority (early occupancy: the sort
+    // chain is the critical path, its pending CTAs go first -- c3 3.17 vs
+    // 3.41 ms; c2/c4 are better without); FMMB_SIDE_PRIO=1: always high
     int lo_prio = 0, hi_prio = 0;
     cudaDeviceGetStreamPriorityRange(&lo_prio, &hi_prio);
     const char* sp = getenv("FMMB_SIDE_PRIO");
     const int prio = (sp && atoi(sp)) ? hi_prio : 0;
-    if (cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, prio) != cudaSuccess) {
+    if (cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, prio) != cudaSuccess ||
+        cudaStreamCreateWithPriority(&side_hi, cudaStreamNonBlocking, hi_prio) != cudaSuccess) {
       cudaFreeHost(h->pinned);
       delete h;
       return FMMB_ERR_CUDA;
     }
+    h->side_hi = side_hi;
     for (auto& x : e) cudaEventCreateWithFlags(&x, cudaEventDisableTiming);
     h->side = side;
     h->ev_split = e[0];
@@ -159,6 +163,7 @@ extern "C" fmmb_status fmmb_destroy(fmmb_handle_t h) {
   cudaSetDevice(h->device);
   if (h->pinned) cudaFreeHost(h->pinned);
   if (h->side) cudaStreamDestroy((cudaStream_t)h->side);
+  if (h->side_hi) cudaStreamDestroy((cudaStream_t)h->side_hi);
   for (void* e : {h->ev_split, h->ev_rank, h->ev_side, h->ev_plan, h->ev_count})
     if (e) cudaEventDestroy((cudaEvent_t)e);
   for (void* e : h->tr_ev)
@@ -703,7 +708,10 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     // the scatter sets the bits itself -- c2: 3.04 vs 3.19 ms)
     const bool early = fast && lists && !dsa && ls != s &&
                        (h->early_occ == 2 || (h->early_occ == 1 && !spec));
-    if (early) spec = false;
+    if (early) {
+      spec = false;
+      ls = (cudaStream_t)h->side_hi;  // the sort chain is the critical path
+    }
     if (tot > 0) {
       const fmmb_status st =
           fast ? sort_bucket(h, src, q, n, recv, m, L, lo, heads, spec, dplan, s, launches, brun,
@@ -734,7 +742,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
 
     // ---- K5: bitmap pyramid (big levels one launch each, the rest in one CTA)
     int l = lists ? L : 0;
-    while (l >= 1 && level_words(l - 1) > 4096) {
+    while (l >= 1 && level_words(l - 1) > 256) {
       const int64_t nc = level_words(l - 1);
       k_pyramid<<<(unsigned)ceil_div(2 * nc, 256), 256, 0, s>>>(
           bmp + rp.word_off[l], bmp + rp.word_off[l - 1], bmp + rp.word_off[stride + l],

@@ -285,7 +285,7 @@ extern "C" fmmb_status fmmb_dist_lists(fmmb_handle_t h, const uint64_t* gbmp, in
                   cudaMemcpyDeviceToDevice, s);
   // coarse levels of the global bitmaps
   int l = L;
-  while (l >= 1 && level_words(l - 1) > 4096) {
+  while (l >= 1 && level_words(l - 1) > 256) {
     const int64_t nc = level_words(l - 1);
     k_pyramid<<<(unsigned)ceil_div(2 * nc, 256), 256, 0, s>>>(
         bmp + rp.word_off[l], bmp + rp.word_off[l - 1], bmp + rp.word_off[stride + l],

@@ -256,22 +256,32 @@ __global__ void __launch_bounds__(kRThreads) k_rank(const __grid_constant__ Rank
   uint64_t r = (uint64_t)s_excl + x + off;
   uint32_t* dir = p.dir + p.word_off[seg];
   uint64_t* keys = p.keys_out[seg];
+  uint64_t rr[kRWordsPerThread];
 #pragma unroll
   for (int i = 0; i < kRWordsPerThread; ++i) {
     const int64_t wl = wl0 + i;
-    if (wl < p.nwords[seg]) {
-      dir[wl] = (uint32_t)r;
-      if (keys) {
-        uint64_t b = w[i];
-        uint64_t j = r;
-        while (b) {
-          const int bit = __ffsll((long long)b) - 1;
-          b &= b - 1;
-          keys[j++] = (uint64_t)wl * 64 + bit;
-        }
+    rr[i] = r;
+    if (wl < p.nwords[seg]) dir[wl] = (uint32_t)r;
+    r += __popcll(w[i]);
+  }
+  if (keys) {
+    // box keys, warp-cooperative: one bitmap word at a time, lane = bits
+    // lane and lane + 32, so a word's keys leave as one coalesced store
+    // (per-thread bit loops wrote 32 scattered streams of up to 256 keys)
+    const uint64_t below_lo = (1ull << lane) - 1ull;
+    const uint64_t below_hi = lane == 31 ? 0x7FFFFFFFFFFFFFFFull : (1ull << (lane + 32)) - 1ull;
+    for (int srcl = 0; srcl < 32; ++srcl) {
+#pragma unroll
+      for (int i = 0; i < kRWordsPerThread; ++i) {
+        const uint64_t b = __shfl_sync(0xffffffffu, w[i], srcl);
+        if (b == 0) continue;  // warp-uniform
+        const uint64_t r0 = __shfl_sync(0xffffffffu, rr[i], srcl);
+        const int64_t wl = wl0 + (int64_t)(srcl - lane) * kRWordsPerThread + i;
+        if ((b >> lane) & 1ull) keys[r0 + __popcll(b & below_lo)] = (uint64_t)wl * 64 + lane;
+        if ((b >> (lane + 32)) & 1ull)
+          keys[r0 + __popcll(b & below_hi)] = (uint64_t)wl * 64 + lane + 32;
       }
     }
-    r += __popcll(w[i]);
   }
 }
 

@@ -21,6 +21,7 @@ struct fmmb_handle_s {
   // the caller's stream builds the directory and the lists (both only need
   // the occupancy bitmaps, which the scatter sets)
   void* side = nullptr;          // cudaStream_t
+  void* side_hi = nullptr;       // cudaStream_t, highest priority (early-occupancy sort chain)
   void* ev_split = nullptr;      // cudaEvent_t: scatter done (caller stream)
   void* ev_rank = nullptr;       // rank directory done (caller stream)
   void* ev_side = nullptr;       // side stream's work done
