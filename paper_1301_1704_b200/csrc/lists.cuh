@@ -377,6 +377,8 @@ struct ListsSmem {  // per-CTA copies of the tables (lane-divergent lookups)
   uint8_t order[48][32];
   uint32_t cand[28 * 8];
   uint32_t slot[kLWarps][2][32];  // per warp: occupied window members, compacted
+  uint32_t dcand[kLWarps][224];    // per warp, dense windows: rank | code base << 32 ...
+  int16_t dcode[kLWarps][224];     // ... split: source rank and code base per candidate
 };
 __device__ __forceinline__ void load_tables(ListsSmem& t) {
   for (int i = threadIdx.x; i < 48 * 32 / 4; i += blockDim.x)
@@ -476,6 +478,21 @@ __device__ __forceinline__ void write_parent(const ListsParams& p, const ListsLa
     int64_t* r4 = p.ranks_out[l] + __ldg(p.bm[l] + rf);
     int16_t* c4 = p.codes_out[l] + __ldg(p.bm[l] + rf);
     int64_t* r2 = l == L ? p.ranks_out[0] + __ldg(p.bm[0] + rf) : nullptr;
+    // per candidate e = slot * 8 + child, once for the 8 rows: source rank
+    // (consecutive children) and code base
+    uint32_t* drk = t.dcand[threadIdx.x >> 5];
+    int16_t* dcd = t.dcode[threadIdx.x >> 5];
+    __syncwarp();  // the previous parent's reads are done
+#pragma unroll
+    for (int k = 0; k < 7; ++k) {
+      const int e = 32 * k + lane;
+      const int sl = e >> 3 < 27 ? e >> 3 : 26;
+      const uint32_t f = __shfl_sync(FULL, sfirst, sl);
+      const int om = __shfl_sync(FULL, o, sl);
+      drk[e] = f + (uint32_t)(e & 7);
+      dcd[e] = (int16_t)(t.cand[om * 8 + (e & 7)] >> 8);
+    }
+    __syncwarp();
 #pragma unroll 1
     for (int cr = 0; cr < 8; ++cr) {
       const int crw = (cr & 1) + 7 * ((cr >> 1) & 1) + 49 * ((cr >> 2) & 1);
@@ -483,21 +500,16 @@ __device__ __forceinline__ void write_parent(const ListsParams& p, const ListsLa
 #pragma unroll
       for (int g = 0; g < 6; ++g) {
         const int tt = 32 * g + lane;
-        const uint32_t e = __ldg(q4 + (tt < kDenseE4 ? tt : 0));
-        const int sl = (int)(e >> 3), cc = (int)(e & 7u);
-        const uint32_t f = __shfl_sync(FULL, sfirst, sl);
-        const int om = __shfl_sync(FULL, o, sl);
         if (tt < kDenseE4) {
-          r4[tt] = (int64_t)(f + (uint32_t)cc);
-          c4[tt] = (int16_t)((int)(t.cand[om * 8 + cc] >> 8) - crw);
+          const uint32_t e = __ldg(q4 + tt);
+          r4[tt] = (int64_t)drk[e];
+          c4[tt] = (int16_t)(dcd[e] - crw);
         }
       }
       r4 += kDenseE4;
       c4 += kDenseE4;
       if (r2) {
-        const uint32_t e = __ldg(&kDense.e2[cs][cr][lane < kDenseE2 ? lane : 0]);
-        const uint32_t f = __shfl_sync(FULL, sfirst, (int)(e >> 3));
-        if (lane < kDenseE2) r2[lane] = (int64_t)(f + (e & 7u));
+        if (lane < kDenseE2) r2[lane] = (int64_t)drk[__ldg(&kDense.e2[cs][cr][lane])];
         r2 += kDenseE2;
       }
     }
