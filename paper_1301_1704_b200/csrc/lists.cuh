@@ -448,7 +448,8 @@ __device__ __forceinline__ void write_parent(const ListsParams& p, const ListsLa
   const unsigned FULL = 0xffffffffu;
   const int c = lane & 7;
   const uint64_t P = __ldg(p.rkeys[l - 1] + lay.p_lo[l] + j);
-  const int o = t.order[window_case(P, l - 1)][lane];
+  const int cs = window_case(P, l - 1);
+  const int o = t.order[cs][lane];
   const uint64_t qk = window_key(P, l, o);
   uint32_t sm = 0, sfirst = 0;
   if (qk != ~0ull)
@@ -458,7 +459,10 @@ __device__ __forceinline__ void write_parent(const ListsParams& p, const ListsLa
   // owned children (a contiguous run of ranks) and the first one's CSR row
   uint32_t own = 0;
   int64_t r0 = -1;
-  {
+  if ((int64_t)rfirst >= lay.r_lo[l] && (int64_t)rfirst + __popc(rm) <= lay.r_hi[l]) {
+    own = rm;  // the whole run is owned (always, single-GPU)
+    r0 = (int64_t)rfirst - lay.r_lo[l];
+  } else {
     int64_t r = rfirst;
 #pragma unroll
     for (int cb = 0; cb < 8; ++cb)
@@ -473,7 +477,6 @@ __device__ __forceinline__ void write_parent(const ListsParams& p, const ListsLa
   if (!own) return;
   if (!COMPACT && l >= 2 && own == 0xFFu &&
       __all_sync(FULL, lane >= 27 || sm == 0xFFu)) {  // dense window (see DenseSeq)
-    const int cs = window_case(P, l - 1);
     const uint32_t rf = (uint32_t)r0;
     int64_t* r4 = p.ranks_out[l] + __ldg(p.bm[l] + rf);
     int16_t* c4 = p.codes_out[l] + __ldg(p.bm[l] + rf);
