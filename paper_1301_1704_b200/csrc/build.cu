@@ -69,7 +69,7 @@ extern "C" fmmb_status fmmb_create(int device, fmmb_handle_t* out) {
   }
   {
     cudaStream_t side, side_hi;
-    cudaEvent_t e[5];
+    cudaEvent_t e[6];
     // two sort streams: default priority (late occupancy: the local pass
     // beside the lists) and the highest priority (early occupancy: the sort
     // chain is the critical path, its pending CTAs go first -- c3 3.17 vs
@@ -92,6 +92,8 @@ extern "C" fmmb_status fmmb_create(int device, fmmb_handle_t* out) {
     h->ev_side = e[2];
     h->ev_plan = e[3];
     h->ev_count = e[4];
+    h->ev_rb = e[5];
+    h->lists_upfront = getenv("FMMB_LISTS_EXACT") == nullptr;
     // early occupancy: the scatter right after the refinement plan (c3 3.16 vs
     // 3.43 ms with it waiting for the list count); FMMB_SCATTER_AFTER_COUNT=1
     h->scatter_after_count = getenv("FMMB_SCATTER_AFTER_COUNT") != nullptr;
@@ -164,7 +166,7 @@ extern "C" fmmb_status fmmb_destroy(fmmb_handle_t h) {
   if (h->pinned) cudaFreeHost(h->pinned);
   if (h->side) cudaStreamDestroy((cudaStream_t)h->side);
   if (h->side_hi) cudaStreamDestroy((cudaStream_t)h->side_hi);
-  for (void* e : {h->ev_split, h->ev_rank, h->ev_side, h->ev_plan, h->ev_count})
+  for (void* e : {h->ev_split, h->ev_rank, h->ev_side, h->ev_plan, h->ev_count, h->ev_rb})
     if (e) cudaEventDestroy((cudaEvent_t)e);
   for (void* e : h->tr_ev)
     if (e) cudaEventDestroy((cudaEvent_t)e);
@@ -690,6 +692,32 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
   auto join = [&]() {
     if (ls != s) cudaStreamWaitEvent(s, (cudaEvent_t)h->ev_side, 0);
   };
+  // Dense geometries (>= 4 points per finest box on average: every row is
+  // full, so the per-row bounds E4 <= 189, E2 <= 27 overshoot the real list
+  // sizes by a few percent): the list arena is allocated up front at those
+  // bounds and the write pass is enqueued right behind the count -- the host
+  // waits for the size read-back only, not before launching the write.
+  const bool upfront = lists && L >= 2 && h->lists_upfront &&
+                       (double)m >= 4.0 * std::ldexp(1.0, 3 * L);
+  if (upfront) {
+    Carver b;
+    const size_t b_e2 = b.take<int64_t>(27 * cap_level(m, L));
+    size_t b_r[kMaxLevel + 1] = {}, b_c[kMaxLevel + 1] = {};
+    for (int k = 2; k <= L; ++k) {
+      b_r[k] = b.take<int64_t>(189 * cap_level(m, k));
+      b_c[k] = b.take<int16_t>(189 * cap_level(m, k));
+    }
+    char* arena_b = (char*)alloc(ctx, std::max<size_t>(b.off, 256));
+    if (!arena_b) {
+      cudaFreeAsync(ws, s);
+      return fmmb_fail(h, FMMB_ERR_ALLOC, "list allocation of %zu bytes failed", b.off);
+    }
+    lp.ranks_out[0] = (int64_t*)(arena_b + b_e2);
+    for (int k = 2; k <= L; ++k) {
+      lp.ranks_out[k] = (int64_t*)(arena_b + b_r[k]);
+      lp.codes_out[k] = (int16_t*)(arena_b + b_c[k]);
+    }
+  }
   for (int attempt = 0;; ++attempt) {
     h->tr_n = 0;
     fmmb_trace_point(h, "start", s);
@@ -856,8 +884,16 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     // occupancy: the sort stream's refinement plan (overflow flag) first
     if (early && tot > 0) cudaStreamWaitEvent(s, (cudaEvent_t)h->ev_plan, 0);
     cudaMemcpyAsync(hp, dplan, sizeof(BuildPlanHost), cudaMemcpyDeviceToHost, s);
+    cudaEventRecord((cudaEvent_t)h->ev_rb, s);
     fmmb_trace_point(h, "size read-back (s)", s);
-    cudaError_t ce = cudaStreamSynchronize(s);
+    if (upfront) {  // the write right behind the count (sizes are not needed for it)
+      if (ev) cudaEventRecord(ev[4], s);
+      launch_lists_write(h, lp, (const ListsLayout*)W(o_lay), nwork_cap, false, s);
+      ++launches;
+      fmmb_trace_point(h, "lists write (s)", s);
+      if (ev) cudaEventRecord(ev[5], s);
+    }
+    cudaError_t ce = cudaEventSynchronize((cudaEvent_t)h->ev_rb);
     if (ce != cudaSuccess) {
       join();
       cudaFreeAsync(ws, s);
@@ -927,6 +963,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
   if (lists) {
     // ---- phase B: exactly-sized list outputs, then the write pass
     const int64_t e2 = hp->seg_totals[0];
+    if (!upfront) {
     Carver b;
     const size_t b_e2 = b.take<int64_t>(e2);
     size_t b_r[kMaxLevel + 1] = {}, b_c[kMaxLevel + 1] = {};
@@ -952,6 +989,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     ++launches;
     fmmb_trace_point(h, "lists write (s)", s);
     if (ev) cudaEventRecord(ev[5], s);  // the write kernel alone (before the side join)
+    }
 
     out->neighbor_bookmark = lp.bm[0];
     out->neighbor_list = lp.ranks_out[0];

@@ -27,6 +27,9 @@ struct fmmb_handle_s {
   void* ev_side = nullptr;       // side stream's work done
   void* ev_plan = nullptr;       // early occupancy: refinement plan done (sort stream)
   void* ev_count = nullptr;      // early occupancy: list count done (caller stream)
+  void* ev_rb = nullptr;         // size read-back done (the host waits on it)
+  bool lists_upfront = true;     // dense geometries: list arena at the row bounds, write
+                                 // enqueued before the host wait (FMMB_LISTS_EXACT=1: off)
   bool scatter_after_count = false;  // early occupancy: scatter waits for the list count
                                     // (FMMB_SCATTER_AFTER_COUNT=1; default: right after the plan)
   int early_occ = 1;             // occupancy bits from the histogram pass, sort on the side
