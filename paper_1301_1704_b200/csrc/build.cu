@@ -299,7 +299,7 @@ void launch_spec(const double* src, const double* q, const double* recv, const B
                  int num_sms, int L, uint32_t* counts, uint32_t* bstart, uint64_t* sst,
                  uint32_t* ctl, uint32_t* rbase, const PlanOut& po, double* rec, uint32_t* idx,
                  uint32_t* spec_fail, uint32_t* err, cudaStream_t s,
-                 unsigned long long* const* sbmp) {
+                 unsigned long long* const* sbmp, std::function<void(cudaStream_t)>* tail) {
   const unsigned nbg = (unsigned)ceil_div(g.nb, 256);
   k_spec_init<<<nbg, 256, 0, s>>>(g, kSpecStride, po.cursor, rbase, po.desc, po.nfinal);
   const int sgrid = (int)std::min<int64_t>(num_sms, ceil_div(g.n + g.m, kSRows));
@@ -309,11 +309,17 @@ void launch_spec(const double* src, const double* q, const double* recv, const B
   fm.bmp[1] = sbmp[1];
   k_bkt_scatter<NARROW><<<(unsigned)sgrid, kSThreads, scatter_smem_bytes(), s>>>(
       src, q, recv, g, L, scatter_rows_per_cta(g.n + g.m, sgrid), po.cursor, rec, idx, fm);
-  k_spec_counts<<<nbg, 256, 0, s>>>(g, kSpecStride, po.cursor, counts);
+  // bucket starts from the final cursors: only the local pass and the heads
+  // need them, so they run on the local pass's stream (the directory starts
+  // right after the scatter)
   BucketGeo g1 = g;
   g1.hgrid = 1;
-  k_bkt_scan<<<(unsigned)ceil_div(g.nb, kScanBuckets), 256, 0, s>>>(counts, g1, bstart, sst,
-                                                                    ctl + 0, ctl + 2);
+  uint32_t* cursor = po.cursor;
+  *tail = [=](cudaStream_t st) {
+    k_spec_counts<<<nbg, 256, 0, st>>>(g, kSpecStride, cursor, counts);
+    k_bkt_scan<<<(unsigned)ceil_div(g.nb, kScanBuckets), 256, 0, st>>>(counts, g1, bstart, sst,
+                                                                       ctl + 0, ctl + 2);
+  };
 }
 
 // Histogram path.  With `early` the histogram pass (on `s`) also sets the
@@ -428,13 +434,14 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
   uint32_t* fine = (uint32_t*)(w + o_fine);
   const bool narrow = L <= 10;
   uint32_t* rbase = spec ? (uint32_t*)(w + o_rb) : nullptr;
+  std::function<void(cudaStream_t)> spec_tail;  // spec path: bucket starts, before the local pass
   if (spec) {  // no histogram pass: fixed regions, exact starts from the final cursors
     if (narrow)
       launch_spec<true>(src, q, recv, g, h->num_sms, L, mat, bstart, sst, ctl, rbase, po, rec,
-                        idx, &dplan->spec_fail, &dplan->err, s, o.bmp);
+                        idx, &dplan->spec_fail, &dplan->err, s, o.bmp, &spec_tail);
     else
       launch_spec<false>(src, q, recv, g, h->num_sms, L, mat, bstart, sst, ctl, rbase, po, rec,
-                         idx, &dplan->spec_fail, &dplan->err, s, o.bmp);
+                         idx, &dplan->spec_fail, &dplan->err, s, o.bmp, &spec_tail);
     po.bstart_f = bstart;
   } else {
     cudaEvent_t evs = (cudaEvent_t)h->ev_split, evp = early ? (cudaEvent_t)h->ev_plan : nullptr;
@@ -469,6 +476,7 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
   // stream's kernels find room (c4: 2.28 vs 2.43 ms per step; c2 even)
   const int lcap = (!early && ls != s) ? 2 : 0;
   auto local = [=](cudaStream_t st) {
+    if (spec_tail) spec_tail(st);
 #define FMMB_LOCAL(CK, NW, HD)                                                                 \
   launch_local<CK, NW, HD>(h, rec, idx, pl.bstart_f, rbase, pl.desc, pl.nfinal, g, L, ol, lst, \
                            lfail, lcap, st)
