@@ -12,3 +12,6 @@ tail -1 gpurun_out/val/bench_official.log | cut -c1-400
 for f in gpurun_out/val/c?.log; do python -c "
 import json
 d=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', round(d['ms_per_step'],3), {k: round(v,3) for k,v in d['phases_ms'].items()})"; done
+timeout 600 python bench.py --impl reference --steps 2 --warmup 0 > gpurun_out/val/bench_ref.log 2>&1
+tail -1 gpurun_out/val/bench_ref.log | cut -c1-600
+timeout 300 python tools/c1_latency.py c1 > gpurun_out/val/c1_latency.log 2>&1; head -2 gpurun_out/val/c1_latency.log
