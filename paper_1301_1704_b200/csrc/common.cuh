@@ -143,6 +143,35 @@ __device__ __forceinline__ uint64_t lookback(const uint64_t* states,
   return excl;
 }
 
+// Same look-back run by one whole warp: lane i polls tile t-1-i of a 32-tile
+// window, the window stops at its nearest inclusive prefix, else every
+// aggregate is added and the window slides 32 tiles back.  One round trip
+// per 32 predecessors instead of one per predecessor.  All lanes return the
+// same value.
+__device__ __forceinline__ uint64_t lookback_warp(const uint64_t* states,
+                                                  int64_t tile, int64_t first_tile,
+                                                  int64_t stride) {
+  const int lane = (int)(threadIdx.x & 31u);
+  uint64_t excl = 0;
+  for (int64_t top = tile - 1; top >= first_tile; top -= 32) {
+    const int64_t t = top - lane;
+    uint64_t s = kStInclusive;  // before the segment: inclusive 0
+    if (t >= first_tile) {
+      do {
+        s = ld_state(states + t * stride);
+      } while ((s & kStMask) == kStInvalid);
+    }
+    const unsigned inc = __ballot_sync(0xffffffffu, (s & kStMask) == kStInclusive);
+    const int stop = inc ? __ffs(inc) - 1 : 31;
+    uint64_t v = lane <= stop ? (s & kStValue) : 0ull;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    excl += v;
+    if (inc) break;
+  }
+  return excl;
+}
+
 // --------------------------------------------------------------- warps ----
 __device__ __forceinline__ unsigned lane_id() { return threadIdx.x & 31u; }
 __device__ __forceinline__ unsigned lanemask_lt() {

@@ -239,18 +239,20 @@ __global__ void __launch_bounds__(kRThreads) k_rank(const __grid_constant__ Rank
     off += i < warp ? s_tmp[i] : 0u;
     tot += s_tmp[i];
   }
-  if (tid == 0) {
+  if (warp == 0) {
     uint64_t* st = p.states + tile;
     uint64_t excl = 0;
     if (tile == first_tile) {
-      st_state(st, kStInclusive | tot);
+      if (lane == 0) st_state(st, kStInclusive | tot);
     } else {
-      st_state(st, kStAggregate | tot);
-      excl = lookback(p.states, tile, first_tile, 1);
-      st_state(st, kStInclusive | (excl + tot));
+      if (lane == 0) st_state(st, kStAggregate | tot);
+      excl = lookback_warp(p.states, tile, first_tile, 1);
+      if (lane == 0) st_state(st, kStInclusive | (excl + tot));
     }
-    s_excl = (int64_t)excl;
-    if (tile == p.tile_off[seg + 1] - 1) p.totals[seg] = (int64_t)(excl + tot);
+    if (lane == 0) {
+      s_excl = (int64_t)excl;
+      if (tile == p.tile_off[seg + 1] - 1) p.totals[seg] = (int64_t)(excl + tot);
+    }
   }
   __syncthreads();
   uint64_t r = (uint64_t)s_excl + x + off;

@@ -692,30 +692,22 @@ __global__ void __launch_bounds__(kLThreads)
     tot2 += s_w2[i];
   }
   const bool last = tile == lay.tile_off[l + 1] - 1;
-  if (tid == 0) {
-    uint64_t e4 = 0, e2 = 0;
-    if (l >= 2) {
-      uint64_t* st = st4 + tile;
+  // warp 0 looks back over the E4 states, warp 1 over the E2 states
+  if (warp < 2) {
+    const bool on = warp == 0 ? l >= 2 : l == L;
+    uint64_t* sts = warp == 0 ? st4 : st2;
+    const uint64_t tot = warp == 0 ? tot4 : tot2;
+    uint64_t e = 0;
+    if (on) {
       if (tile == first_tile) {
-        st_state(st, kStInclusive | tot4);
+        if (lane == 0) st_state(sts + tile, kStInclusive | tot);
       } else {
-        st_state(st, kStAggregate | tot4);
-        e4 = lookback(st4, tile, first_tile, 1);
-        st_state(st, kStInclusive | (e4 + tot4));
+        if (lane == 0) st_state(sts + tile, kStAggregate | tot);
+        e = lookback_warp(sts, tile, first_tile, 1);
+        if (lane == 0) st_state(sts + tile, kStInclusive | (e + tot));
       }
     }
-    if (l == L) {
-      uint64_t* st = st2 + tile;
-      if (tile == first_tile) {
-        st_state(st, kStInclusive | tot2);
-      } else {
-        st_state(st, kStAggregate | tot2);
-        e2 = lookback(st2, tile, first_tile, 1);
-        st_state(st, kStInclusive | (e2 + tot2));
-      }
-    }
-    s_b4 = (int64_t)e4;
-    s_b2 = (int64_t)e2;
+    if (lane == 0) (warp == 0 ? s_b4 : s_b2) = (int64_t)e;
   }
   __syncthreads();
   const int64_t base4 = s_b4, base2 = s_b2;
