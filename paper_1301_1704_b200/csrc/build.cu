@@ -109,6 +109,7 @@ extern "C" fmmb_status fmmb_create(int device, fmmb_handle_t* out) {
     h->local_after_count = getenv("FMMB_LOCAL_AFTER") != nullptr;
     const char* lc = getenv("FMMB_LC_PER_SM");
     h->lc_per_sm = lc ? atoi(lc) : 0;
+    h->dense_rows = getenv("FMMB_DENSE_ROWS") != nullptr;
   }
   // stream-ordered pool: keep freed workspace for reuse across calls
   cudaMemPool_t pool;
@@ -830,6 +831,7 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
     nwork_cap = 0;
     if (lists) {
       lp.level = L;
+      lp.dense_rows = h->dense_rows;
       lp.key_lo = 0;
       lp.key_hi = 1ull << (3 * L);
       lp.ktot = dplan->ktot;

@@ -39,6 +39,7 @@ struct ListsParams {
   // grid for a single-GPU build; a Morton range under the multi-GPU
   // partition).  A level-l box is owned when its first finest-level key is.
   uint64_t key_lo, key_hi;
+  int dense_rows;  // A/B knob: dense windows written row by row (no line alignment)
 };
 
 // Per-level work and segment layout, recomputed per block from the device
@@ -343,42 +344,113 @@ __constant__ CandTable kCand = CandTable();
 // owned (c2: ~85 % of the finest-level parents), every row's output is a
 // fixed sequence: E4 = the 189 candidates outside the child's own window,
 // E2 = the 27 inside, in (member slot, child) order, with consecutive source
-// ranks per member.  The sequences depend only on the window case and the
-// child, so they are tabulated (entry = slot * 8 + child) and a row is
-// written lane = output entry: no ballots, no compaction.
+// ranks per member.  The 8 rows of the parent are consecutive in the CSR
+// output, so the parent's whole E4 (E2) output is ONE run of 8 x 189 (8 x 27)
+// entries whose candidate sequence and codes depend only on the window case:
+// tabulated here (entry = slot * 8 + child), written as line-aligned vector
+// stores (dense_run) -- no ballots, no compaction, no partial lines inside a
+// run.
+constexpr int kDenseE4 = 189, kDenseE2 = 27;
 struct DenseSeq {
-  uint8_t e4[48][8][192];
-  uint8_t e2[48][8][32];
+  uint8_t e4[48][8 * kDenseE4];
+  uint8_t e2[48][8 * kDenseE2];
   constexpr DenseSeq() : e4(), e2() {
     const WinOrder wo;
-    for (int cs = 0; cs < 48; ++cs)
-      for (int cr = 0; cr < 8; ++cr) {
-        int k4 = 0, k2 = 0;
-        for (int sl = 0; sl < 27; ++sl) {
-          const int o = wo.o[cs][sl];
-          const int off[3] = {o % 3 - 1, (o / 3) % 3 - 1, o / 9 - 1};
+    const CandTable ct;
+    for (int cs = 0; cs < 48; ++cs) {
+      int k4 = 0, k2 = 0;
+      for (int cr = 0; cr < 8; ++cr)
+        for (int sl = 0; sl < 27; ++sl)
           for (int c = 0; c < 8; ++c) {
-            bool near = true;
-            for (int a = 0; a < 3; ++a) {
-              const int d = 2 * off[a] + ((c >> a) & 1) - ((cr >> a) & 1);
-              near = near && d >= -1 && d <= 1;
-            }
-            if (near) e2[cs][cr][k2++] = (uint8_t)(sl * 8 + c);
-            else e4[cs][cr][k4++] = (uint8_t)(sl * 8 + c);
+            if ((ct.v[wo.o[cs][sl] * 8 + c] >> cr) & 1u)
+              e2[cs][k2++] = (uint8_t)(sl * 8 + c);
+            else
+              e4[cs][k4++] = (uint8_t)(sl * 8 + c);
           }
-        }
-      }
+    }
   }
 };
 __device__ const DenseSeq kDense = DenseSeq();
-constexpr int kDenseE4 = 189, kDenseE2 = 27;
+
+__device__ __forceinline__ void st_v2_s64(int64_t* p, int64_t a, int64_t b) {
+  asm volatile("st.global.v2.s64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
+}
+
+// code offset of child receiver cr (c_x + 7 c_y + 49 c_z), 6 bits per cr
+constexpr uint64_t kCrw = 0ull | (1ull << 6) | (7ull << 12) | (8ull << 18) | (49ull << 24) |
+                          (50ull << 30) | (56ull << 36) | (57ull << 42);
+__device__ __forceinline__ int16_t dense_code(const int16_t* dcd, uint32_t e, int k) {
+  const int cr = (k * 5549) >> 20;  // k / 189 for k < 1512
+  return (int16_t)(dcd[e] - (int)((kCrw >> (6 * cr)) & 63u));
+}
+
+// One dense run of n entries: rank = drk[e[k]] (+ its E4 code when CODES:
+// the candidate's code base dcd[e] minus the row's child offset).
+// Lane pairs (k, k+1) are laid over the output so that every warp store
+// covers whole 128-B lines: 64 entries per step = 512 B of ranks in four
+// lines (16-B pair stores) and 128 B of codes in one line (4-B pair
+// stores); only the first and last lines of the run are partial.
+template <bool CODES>
+__device__ __forceinline__ void dense_run(int64_t* __restrict__ r, int16_t* __restrict__ c,
+                                          const uint8_t* __restrict__ et, int n,
+                                          const uint32_t* __restrict__ drk,
+                                          const int16_t* __restrict__ dcd, int lane) {
+  const uintptr_t ra = (uintptr_t)r >> 3;
+  const uintptr_t ca = CODES ? (uintptr_t)c >> 1 : ra;
+  const int a = (int)(ca & 63);            // entries before the run in its line
+  const bool pair = ((ra ^ ca) & 1) == 0;  // rank pairs 16-B aligned (warp-uniform)
+  const int nit = (n + a + 63) >> 6;
+  constexpr int U = 4;  // steps in flight: table loads, then shared loads, then stores
+  for (int it0 = 0; it0 < nit; it0 += U) {
+    uint32_t e0[U], e1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k0 = 2 * lane - a + 64 * (it0 + u);
+      const int q0 = min(max(k0, 0), n - 1), q1 = min(max(k0 + 1, 0), n - 1);
+      e0[u] = __ldg(et + q0);
+      e1[u] = __ldg(et + q1);
+    }
+    int64_t v0[U], v1[U];
+    int16_t w0[U], w1[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k0 = 2 * lane - a + 64 * (it0 + u);
+      v0[u] = (int64_t)drk[e0[u]];
+      v1[u] = (int64_t)drk[e1[u]];
+      if (CODES) {
+        w0[u] = dense_code(dcd, e0[u], min(max(k0, 0), n - 1));
+        w1[u] = dense_code(dcd, e1[u], min(max(k0 + 1, 0), n - 1));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int k0 = 2 * lane - a + 64 * (it0 + u), k1 = k0 + 1;
+      const bool ok0 = k0 >= 0 && k0 < n, ok1 = k1 >= 0 && k1 < n;
+      if (ok0 && ok1 && pair) {
+        st_v2_s64(r + k0, v0[u], v1[u]);
+      } else {
+        if (ok0) r[k0] = v0[u];
+        if (ok1) r[k1] = v1[u];
+      }
+      if (CODES) {
+        if (ok0 && ok1) {
+          *reinterpret_cast<uint32_t*>(c + k0) =
+              (uint32_t)(uint16_t)w0[u] | ((uint32_t)(uint16_t)w1[u] << 16);
+        } else {
+          if (ok0) c[k0] = w0[u];
+          if (ok1) c[k1] = w1[u];
+        }
+      }
+    }
+  }
+}
 
 struct ListsSmem {  // per-CTA copies of the tables (lane-divergent lookups)
   uint8_t order[48][32];
   uint32_t cand[28 * 8];
   uint32_t slot[kLWarps][2][32];  // per warp: occupied window members, compacted
-  uint32_t dcand[kLWarps][224];    // per warp, dense windows: rank | code base << 32 ...
-  int16_t dcode[kLWarps][224];     // ... split: source rank and code base per candidate
+  uint32_t dcand[kLWarps][224];    // per warp, dense windows: source rank per candidate ...
+  int16_t dcode[kLWarps][224];     // ... and its E4 code base
 };
 __device__ __forceinline__ void load_tables(ListsSmem& t) {
   for (int i = threadIdx.x; i < 48 * 32 / 4; i += blockDim.x)
@@ -478,11 +550,10 @@ __device__ __forceinline__ void write_parent(const ListsParams& p, const ListsLa
   if (!COMPACT && l >= 2 && own == 0xFFu &&
       __all_sync(FULL, lane >= 27 || sm == 0xFFu)) {  // dense window (see DenseSeq)
     const uint32_t rf = (uint32_t)r0;
-    int64_t* r4 = p.ranks_out[l] + __ldg(p.bm[l] + rf);
-    int16_t* c4 = p.codes_out[l] + __ldg(p.bm[l] + rf);
-    int64_t* r2 = l == L ? p.ranks_out[0] + __ldg(p.bm[0] + rf) : nullptr;
+    const int64_t g4 = __ldg(p.bm[l] + rf);
+    const int64_t g2 = l == L ? __ldg(p.bm[0] + rf) : 0;
     // per candidate e = slot * 8 + child, once for the 8 rows: source rank
-    // (consecutive children) and code base
+    // (consecutive children)
     uint32_t* drk = t.dcand[threadIdx.x >> 5];
     int16_t* dcd = t.dcode[threadIdx.x >> 5];
     __syncwarp();  // the previous parent's reads are done
@@ -490,32 +561,41 @@ __device__ __forceinline__ void write_parent(const ListsParams& p, const ListsLa
     for (int k = 0; k < 7; ++k) {
       const int e = 32 * k + lane;
       const int sl = e >> 3 < 27 ? e >> 3 : 26;
-      const uint32_t f = __shfl_sync(FULL, sfirst, sl);
-      const int om = __shfl_sync(FULL, o, sl);
-      drk[e] = f + (uint32_t)(e & 7);
-      dcd[e] = (int16_t)(t.cand[om * 8 + (e & 7)] >> 8);
+      drk[e] = __shfl_sync(FULL, sfirst, sl) + (uint32_t)(e & 7);
+      dcd[e] = (int16_t)(t.cand[__shfl_sync(FULL, o, sl) * 8 + (e & 7)] >> 8);
     }
     __syncwarp();
+    if (p.dense_rows) {
+      int64_t* r4 = p.ranks_out[l] + g4;
+      int16_t* c4 = p.codes_out[l] + g4;
+      int64_t* r2 = l == L ? p.ranks_out[0] + g2 : nullptr;
 #pragma unroll 1
-    for (int cr = 0; cr < 8; ++cr) {
-      const int crw = (cr & 1) + 7 * ((cr >> 1) & 1) + 49 * ((cr >> 2) & 1);
-      const uint8_t* q4 = &kDense.e4[cs][cr][0];
+      for (int cr = 0; cr < 8; ++cr) {
+        const int crw = (cr & 1) + 7 * ((cr >> 1) & 1) + 49 * ((cr >> 2) & 1);
+        const uint8_t* q4 = &kDense.e4[cs][cr * kDenseE4];
 #pragma unroll
-      for (int g = 0; g < 6; ++g) {
-        const int tt = 32 * g + lane;
-        if (tt < kDenseE4) {
-          const uint32_t e = __ldg(q4 + tt);
-          r4[tt] = (int64_t)drk[e];
-          c4[tt] = (int16_t)(dcd[e] - crw);
+        for (int g = 0; g < 6; ++g) {
+          const int tt = 32 * g + lane;
+          if (tt < kDenseE4) {
+            const uint32_t e = __ldg(q4 + tt);
+            r4[tt] = (int64_t)drk[e];
+            c4[tt] = (int16_t)(dcd[e] - crw);
+          }
+        }
+        r4 += kDenseE4;
+        c4 += kDenseE4;
+        if (r2) {
+          if (lane < kDenseE2) r2[lane] = (int64_t)drk[__ldg(&kDense.e2[cs][cr * kDenseE2 + lane])];
+          r2 += kDenseE2;
         }
       }
-      r4 += kDenseE4;
-      c4 += kDenseE4;
-      if (r2) {
-        if (lane < kDenseE2) r2[lane] = (int64_t)drk[__ldg(&kDense.e2[cs][cr][lane])];
-        r2 += kDenseE2;
-      }
+      return;
     }
+    dense_run<true>(p.ranks_out[l] + g4, p.codes_out[l] + g4, kDense.e4[cs], 8 * kDenseE4, drk,
+                    dcd, lane);
+    if (l == L)
+      dense_run<false>(p.ranks_out[0] + g2, nullptr, kDense.e2[cs], 8 * kDenseE2, drk, dcd,
+                       lane);
     return;
   }
   // occupied members compacted in key order (sparse windows -- surfaces,

@@ -1,0 +1,10 @@
+set -x
+D=gpurun_out/${Q:-q18}
+mkdir -p $D
+B="python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e --no-nf --workload"
+for w in c2 c4 c2; do timeout 300 $B $w > $D/$w.log 2>&1; python -c "
+import json
+d=json.loads(open('$D/$w.log').read().strip().splitlines()[-1]); print('$w', round(d['ms_per_step'],3), {k: round(v,3) for k,v in d['phases_ms'].items()})"; done
+FMMB_TRACE=1 timeout 300 python tools/trace_build.py c2 > $D/trace_c2.log 2>&1; tail -11 $D/trace_c2.log
+for w in c2; do timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_write.sum,smsp__inst_executed.sum --clock-control none -k regex:"k_lists_write|k_bkt_local" --csv --log-file $D/l_$w.csv python tools/profile_build.py $w 1 > /dev/null 2>&1; python tools/launches.py $D/l_$w.csv | tail -4; done
+timeout 1200 python -m pytest tests/test_gpu_northstar.py -q -x 2>&1 | tail -2

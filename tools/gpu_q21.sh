@@ -1,0 +1,13 @@
+# A/B: line-aligned list writer (dense runs + staged general rows) vs row-by-row, c2/c3/c4 in-step, write alone
+D=gpurun_out/${Q:-q21}
+mkdir -p $D
+B="python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e --no-nf --workload"
+run() { tag=$1; shift; for w in c2 c3 c4; do env "$@" timeout 300 $B $w > $D/${tag}_$w.log 2>&1; python -c "
+import json
+d=json.loads(open('$D/${tag}_$w.log').read().strip().splitlines()[-1]); print('$tag $w', round(d['ms_per_step'],3), {k: round(v,3) for k,v in d['phases_ms'].items()})"; done; }
+for rep in 1 2; do
+run new X=1
+run rows FMMB_DENSE_ROWS=1
+done
+for w in c2 c3 c4; do timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_write.sum,smsp__inst_executed.sum --clock-control none -k regex:"k_lists_write" --csv --log-file $D/l_$w.csv python tools/profile_build.py $w 1 > /dev/null 2>&1; python tools/launches.py $D/l_$w.csv | tail -3 | head -1; done
+timeout 1200 python -m pytest tests/test_gpu_build_parity.py tests/test_gpu_northstar.py -q -x 2>&1 | tail -2
