@@ -848,8 +848,14 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
           1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * 16));
       ListsLayout* glay = (ListsLayout*)W(o_lay);
       k_lists_plan<<<1, 32, 0, s>>>(lp, glay);
-      k_lists_cscan<<<(unsigned)cs_tiles, kLThreads, 0, s>>>(
-          lp, glay, (uint64_t*)W(o_st4), (uint64_t*)W(o_st2), tc + 10, dplan->seg_totals);
+      // a loose tile bound (deep, sparse levels) gets a persistent grid
+      const bool cs_loop = cs_tiles > (int64_t)h->num_sms * 32;
+      if (cs_loop)
+        k_lists_cscan<true><<<(unsigned)(h->num_sms * 8), kLThreads, 0, s>>>(
+            lp, glay, (uint64_t*)W(o_st4), (uint64_t*)W(o_st2), tc + 10, dplan->seg_totals);
+      else
+        k_lists_cscan<false><<<(unsigned)cs_tiles, kLThreads, 0, s>>>(
+            lp, glay, (uint64_t*)W(o_st4), (uint64_t*)W(o_st2), tc + 10, dplan->seg_totals);
       launches += 2;
       fmmb_trace_point(h, "lists count (s)", s);
     }

@@ -361,9 +361,8 @@ extern "C" fmmb_status fmmb_dist_lists(fmmb_handle_t h, const uint64_t* gbmp, in
   lp.bm[0] = (int64_t*)(arena + a_bm[0]);
   for (int k = 2; k <= L; ++k) lp.bm[k] = (int64_t*)(arena + a_bm[k]);
   k_lists_plan<<<1, 32, 0, s>>>(lp, glay);
-  k_lists_cscan<<<(unsigned)std::max<int64_t>(1, h1.lay.tile_off[L + 1]), kLThreads, 0, s>>>(
-      lp, glay, (uint64_t*)W(o_st4),
-                                                         (uint64_t*)W(o_st2), tc + 2, seg_totals);
+  k_lists_cscan<false><<<(unsigned)std::max<int64_t>(1, h1.lay.tile_off[L + 1]), kLThreads, 0, s>>>(
+      lp, glay, (uint64_t*)W(o_st4), (uint64_t*)W(o_st2), tc + 2, seg_totals);
   h->launches += 2;
   cudaMemcpyAsync(hp->seg_totals, seg_totals, sizeof(hp->seg_totals), cudaMemcpyDeviceToHost, s);
   if (cudaStreamSynchronize(s) != cudaSuccess) return fail(FMMB_ERR_CUDA, "dist_lists phase 2");

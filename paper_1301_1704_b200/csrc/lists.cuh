@@ -692,6 +692,7 @@ __global__ void __launch_bounds__(kLThreads, FMMB_LW_MINB)
 // receiver keys) are scanned in shared memory and offset by a decoupled
 // look-back over the level's tiles (tickets keep tiles in order).  Writes
 // the bookmark arrays and the per-level totals.
+template <bool PERSISTENT>
 __global__ void __launch_bounds__(kLThreads)
     k_lists_cscan(const __grid_constant__ ListsParams p, const ListsLayout* __restrict__ glay,
                   uint64_t* __restrict__ st4, uint64_t* __restrict__ st2,
@@ -703,9 +704,13 @@ __global__ void __launch_bounds__(kLThreads)
   __shared__ int64_t s_tile, s_b4, s_b2;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   load_layout(glay, lay);
+  const int L = p.level;
+  // one tile per CTA, or (PERSISTENT: the per-level bounds the grid is sized
+  // from before the totals are known are loose -- c3: 300 K bound tiles, 5 K
+  // real ones) tiles taken by ticket until none is left
+  for (;;) {
   if (tid == 0) s_tile = atomicAdd(ticket, 1u);
   __syncthreads();
-  const int L = p.level;
   const int64_t tile = s_tile;
   if (L == 0) {  // the root receiver sees the root source
     if (tile == 0 && tid == 0) {
@@ -814,6 +819,9 @@ __global__ void __launch_bounds__(kLThreads)
       p.bm[0][kr] = base2 + tot2;
       seg_totals[0] = base2 + tot2;
     }
+  }
+  if (!PERSISTENT) return;
+  __syncthreads();  // shared state reused by the next tile
   }
 }
 

@@ -1,0 +1,7 @@
+D=gpurun_out/${Q:-q23}
+mkdir -p $D
+B="python bench.py --steps 20 --warmup 5 --no-cpu --no-e2e --no-nf --workload"
+for w in c2 c3 c4 c2 c3; do timeout 300 $B $w > $D/$w.log 2>&1; python -c "
+import json
+d=json.loads(open('$D/$w.log').read().strip().splitlines()[-1]); print('$w', round(d['ms_per_step'],3), {k: round(v,3) for k,v in d['phases_ms'].items()})"; done
+timeout 600 python -m pytest tests/test_gpu_northstar.py -q -x 2>&1 | tail -2
