@@ -15,3 +15,6 @@ d=json.loads(open('$f').read().strip().splitlines()[-1]); print('$f', round(d['m
 timeout 600 python bench.py --impl reference --steps 2 --warmup 0 > gpurun_out/val/bench_ref.log 2>&1
 tail -1 gpurun_out/val/bench_ref.log | cut -c1-600
 timeout 300 python tools/c1_latency.py c1 > gpurun_out/val/c1_latency.log 2>&1; head -2 gpurun_out/val/c1_latency.log
+timeout 600 python tools/c4_trajectory.py > gpurun_out/val/c4_trajectory.log 2>&1; tail -1 gpurun_out/val/c4_trajectory.log | cut -c1-400
+for w in c2 c3 c4; do FMMB_TRACE=1 timeout 300 python tools/trace_build.py $w > gpurun_out/val/trace_$w.log 2>&1; done
+for w in c3 c4; do timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/val/launches_$w.csv python tools/profile_build.py $w 1 > /dev/null 2>&1; done
