@@ -351,14 +351,15 @@ __constant__ CandTable kCand = CandTable();
 // stores (dense_run) -- no ballots, no compaction, no partial lines inside a
 // run.
 constexpr int kDenseE4 = 189, kDenseE2 = 27;
+constexpr int kDensePad = 64;  // table padding: a lane pair's out-of-run index reads a valid 0
 struct DenseSeq {
-  uint8_t e4[48][8 * kDenseE4];
-  uint8_t e2[48][8 * kDenseE2];
+  uint8_t e4[48][kDensePad + 8 * kDenseE4 + kDensePad];
+  uint8_t e2[48][kDensePad + 8 * kDenseE2 + kDensePad];
   constexpr DenseSeq() : e4(), e2() {
     const WinOrder wo;
     const CandTable ct;
     for (int cs = 0; cs < 48; ++cs) {
-      int k4 = 0, k2 = 0;
+      int k4 = kDensePad, k2 = kDensePad;
       for (int cr = 0; cr < 8; ++cr)
         for (int sl = 0; sl < 27; ++sl)
           for (int c = 0; c < 8; ++c) {
@@ -376,12 +377,9 @@ __device__ __forceinline__ void st_v2_s64(int64_t* p, int64_t a, int64_t b) {
   asm volatile("st.global.v2.s64 [%0], {%1, %2};" ::"l"(p), "l"(a), "l"(b) : "memory");
 }
 
-// code offset of child receiver cr (c_x + 7 c_y + 49 c_z), 6 bits per cr
-constexpr uint64_t kCrw = 0ull | (1ull << 6) | (7ull << 12) | (8ull << 18) | (49ull << 24) |
-                          (50ull << 30) | (56ull << 36) | (57ull << 42);
-__device__ __forceinline__ int16_t dense_code(const int16_t* dcd, uint32_t e, int k) {
-  const int cr = (k * 5549) >> 20;  // k / 189 for k < 1512
-  return (int16_t)(dcd[e] - (int)((kCrw >> (6 * cr)) & 63u));
+// code offset of child receiver cr: c_x + 7 c_y + 49 c_z
+__device__ __forceinline__ int crw_of(int cr) {
+  return (cr & 1) + 7 * ((cr >> 1) & 1) + 49 * ((cr >> 2) & 1);
 }
 
 // One dense run of n entries: rank = drk[e[k]] (+ its E4 code when CODES:
@@ -400,26 +398,40 @@ __device__ __forceinline__ void dense_run(int64_t* __restrict__ r, int16_t* __re
   const int a = (int)(ca & 63);            // entries before the run in its line
   const bool pair = ((ra ^ ca) & 1) == 0;  // rank pairs 16-B aligned (warp-uniform)
   const int nit = (n + a + 63) >> 6;
+  et += kDensePad;  // padded table: indices -64 .. n + 63 are readable
+  // E4 row of the pair's first entry, tracked as the pair advances 64
+  // entries a step (< 189: at most one row boundary per step)
+  int cr = (max(2 * lane - a, 0) * 5549) >> 20;  // k / 189 for k < 1512
+  int nb = kDenseE4 * (cr + 1);
+  int crw = crw_of(cr), crwn = crw_of(cr + 1);
   constexpr int U = 4;  // steps in flight: table loads, then shared loads, then stores
   for (int it0 = 0; it0 < nit; it0 += U) {
     uint32_t e0[U], e1[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int k0 = 2 * lane - a + 64 * (it0 + u);
-      const int q0 = min(max(k0, 0), n - 1), q1 = min(max(k0 + 1, 0), n - 1);
-      e0[u] = __ldg(et + q0);
-      e1[u] = __ldg(et + q1);
+      e0[u] = e1[u] = 0;
+      if (it0 + u < nit) {  // (warp-uniform) steps past the run read nothing
+        e0[u] = __ldg(et + k0);
+        e1[u] = __ldg(et + k0 + 1);
+      }
     }
     int64_t v0[U], v1[U];
     int16_t w0[U], w1[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-      const int k0 = 2 * lane - a + 64 * (it0 + u);
       v0[u] = (int64_t)drk[e0[u]];
       v1[u] = (int64_t)drk[e1[u]];
       if (CODES) {
-        w0[u] = dense_code(dcd, e0[u], min(max(k0, 0), n - 1));
-        w1[u] = dense_code(dcd, e1[u], min(max(k0 + 1, 0), n - 1));
+        const int k0 = 2 * lane - a + 64 * (it0 + u);
+        if (k0 >= nb) {
+          ++cr;
+          nb += kDenseE4;
+          crw = crwn;
+          crwn = crw_of(cr + 1);
+        }
+        w0[u] = (int16_t)(dcd[e0[u]] - crw);
+        w1[u] = (int16_t)(dcd[e1[u]] - (k0 + 1 == nb ? crwn : crw));
       }
     }
 #pragma unroll
@@ -572,7 +584,7 @@ __device__ __forceinline__ void write_parent(const ListsParams& p, const ListsLa
 #pragma unroll 1
       for (int cr = 0; cr < 8; ++cr) {
         const int crw = (cr & 1) + 7 * ((cr >> 1) & 1) + 49 * ((cr >> 2) & 1);
-        const uint8_t* q4 = &kDense.e4[cs][cr * kDenseE4];
+        const uint8_t* q4 = &kDense.e4[cs][kDensePad + cr * kDenseE4];
 #pragma unroll
         for (int g = 0; g < 6; ++g) {
           const int tt = 32 * g + lane;
@@ -585,7 +597,7 @@ __device__ __forceinline__ void write_parent(const ListsParams& p, const ListsLa
         r4 += kDenseE4;
         c4 += kDenseE4;
         if (r2) {
-          if (lane < kDenseE2) r2[lane] = (int64_t)drk[__ldg(&kDense.e2[cs][cr * kDenseE2 + lane])];
+          if (lane < kDenseE2) r2[lane] = (int64_t)drk[__ldg(&kDense.e2[cs][kDensePad + cr * kDenseE2 + lane])];
           r2 += kDenseE2;
         }
       }
