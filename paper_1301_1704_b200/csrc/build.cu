@@ -109,6 +109,8 @@ extern "C" fmmb_status fmmb_create(int device, fmmb_handle_t* out) {
     h->local_after_count = getenv("FMMB_LOCAL_AFTER") != nullptr;
     const char* lc = getenv("FMMB_LC_PER_SM");
     h->lc_per_sm = lc ? atoi(lc) : 0;
+    const char* lw = getenv("FMMB_LW_PER_SM");  // list-write CTAs per SM in the grid (A/B)
+    h->lw_per_sm = lw ? std::max(1, atoi(lw)) : 32;
     h->dense_rows = getenv("FMMB_DENSE_ROWS") != nullptr;
   }
   // stream-ordered pool: keep freed workspace for reuse across calls
@@ -573,7 +575,7 @@ fmmb_status sort_onesweep(fmmb_handle_t h, const double* src, const double* q, i
 inline void launch_lists_write(fmmb_handle_t h, const ListsParams& lp, const ListsLayout* lay,
                                int64_t nwork_cap, bool sparse, cudaStream_t s) {
   const int lgrid = (int)std::max<int64_t>(
-      1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * 16));
+      1, std::min<int64_t>(ceil_div(nwork_cap, kLWarps), (int64_t)h->num_sms * h->lw_per_sm));
   if (sparse) k_lists_write<true><<<lgrid, kLThreads, 0, s>>>(lp, lay);
   else k_lists_write<false><<<lgrid, kLThreads, 0, s>>>(lp, lay);
 }

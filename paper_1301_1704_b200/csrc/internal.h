@@ -44,6 +44,7 @@ struct fmmb_handle_s {
   bool local_after_count = false;  // FMMB_LOCAL_AFTER=1: local pass after the list count (A/B)
   int lc_per_sm = 0;   // FMMB_LC_PER_SM: cap on resident local-pass CTAs per SM (A/B)
   int dense_rows = 0;  // FMMB_DENSE_ROWS: row-by-row dense list writer (A/B)
+  int lw_per_sm = 32;  // FMMB_LW_PER_SM: list-write grid in CTAs per SM (A/B)
   // FMMB_TRACE=1: timing events at the phase boundaries of both streams of
   // the last build (fmmb_trace): the overlap timeline without a profiler
   bool trace = false;
