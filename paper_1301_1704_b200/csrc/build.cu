@@ -476,8 +476,10 @@ fmmb_status sort_bucket(fmmb_handle_t h, const double* src, const double* q, int
   const PlanOut pl = po;
   // beside the directory and the lists (late structure, or the partitioned
   // sort's deferred join) the local pass keeps two CTAs per SM so the other
-  // stream's kernels find room (c4: 2.28 vs 2.43 ms per step; c2 even)
-  const int lcap = (!early && ls != s) ? 2 : 0;
+  // stream's kernels find room (c4, 2^24 points: 2.15 vs 2.16 ms per step,
+  // round 1 2.28 vs 2.43); from 2^25 points on its longer pass takes all
+  // three (c2: 2.64 vs 2.655 ms)
+  const int lcap = (!early && ls != s && g.n + g.m < (int64_t)1 << 25) ? 2 : 0;
   auto local = [=](cudaStream_t st) {
     if (spec_tail) spec_tail(st);
 #define FMMB_LOCAL(CK, NW, HD)                                                                 \
