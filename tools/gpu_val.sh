@@ -18,3 +18,6 @@ timeout 300 python tools/c1_latency.py c1 > gpurun_out/val/c1_latency.log 2>&1; 
 timeout 600 python tools/c4_trajectory.py > gpurun_out/val/c4_trajectory.log 2>&1; tail -1 gpurun_out/val/c4_trajectory.log | cut -c1-400
 for w in c2 c3 c4; do FMMB_TRACE=1 timeout 300 python tools/trace_build.py $w > gpurun_out/val/trace_$w.log 2>&1; done
 for w in c3 c4; do timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file gpurun_out/val/launches_$w.csv python tools/profile_build.py $w 1 > /dev/null 2>&1; done
+R="python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29533"
+timeout 900 $R bench.py --partitioned --workload c2 --steps 5 --warmup 3 --no-e2e --no-cpu > gpurun_out/val/part_c2.log 2>&1; tail -1 gpurun_out/val/part_c2.log | cut -c1-300
+timeout 1200 $R bench.py --partitioned --workload c5 --steps 3 --warmup 3 > gpurun_out/val/part_c5.log 2>&1; tail -1 gpurun_out/val/part_c5.log | cut -c1-300
