@@ -109,6 +109,8 @@ extern "C" fmmb_status fmmb_create(int device, fmmb_handle_t* out) {
     h->local_after_count = getenv("FMMB_LOCAL_AFTER") != nullptr;
     const char* lc = getenv("FMMB_LC_PER_SM");
     h->lc_per_sm = lc ? atoi(lc) : 0;
+    const char* csp = getenv("FMMB_CS_PER_SM");  // persistent list-count grid (A/B)
+    h->cs_per_sm = csp ? atoi(csp) : 0;
     const char* lw = getenv("FMMB_LW_PER_SM");  // list-write CTAs per SM in the grid (A/B)
     h->lw_per_sm = lw ? std::max(1, atoi(lw)) : 32;
     h->dense_rows = getenv("FMMB_DENSE_ROWS") != nullptr;
@@ -853,9 +855,10 @@ fmmb_status build_impl(fmmb_handle_t h, const double* src, const double* q, int6
       ListsLayout* glay = (ListsLayout*)W(o_lay);
       k_lists_plan<<<1, 32, 0, s>>>(lp, glay);
       // a loose tile bound (deep, sparse levels) gets a persistent grid
-      const bool cs_loop = cs_tiles > (int64_t)h->num_sms * 32;
+      const bool cs_loop = h->cs_per_sm > 0 || cs_tiles > (int64_t)h->num_sms * 32;
       if (cs_loop)
-        k_lists_cscan<true><<<(unsigned)(h->num_sms * 8), kLThreads, 0, s>>>(
+        k_lists_cscan<true><<<(unsigned)(h->num_sms * (h->cs_per_sm > 0 ? h->cs_per_sm : 8)),
+                              kLThreads, 0, s>>>(
             lp, glay, (uint64_t*)W(o_st4), (uint64_t*)W(o_st2), tc + 10, dplan->seg_totals);
       else
         k_lists_cscan<false><<<(unsigned)cs_tiles, kLThreads, 0, s>>>(

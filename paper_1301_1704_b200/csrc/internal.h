@@ -45,6 +45,7 @@ struct fmmb_handle_s {
   int lc_per_sm = 0;   // FMMB_LC_PER_SM: cap on resident local-pass CTAs per SM (A/B)
   int dense_rows = 0;  // FMMB_DENSE_ROWS: row-by-row dense list writer (A/B)
   int lw_per_sm = 32;  // FMMB_LW_PER_SM: list-write grid in CTAs per SM (A/B)
+  int cs_per_sm = 0;   // FMMB_CS_PER_SM: force the persistent list count at this many CTAs per SM
   // FMMB_TRACE=1: timing events at the phase boundaries of both streams of
   // the last build (fmmb_trace): the overlap timeline without a profiler
   bool trace = false;
